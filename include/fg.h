@@ -1,0 +1,185 @@
+/*
+ * fg.h -- C ABI of libfg.so, the B200 (sm_100a) flip-graph walker of
+ * arXiv 2511.20317 ("FlipGraphGPU"; PAPER.md lines cited as PAPER:<line>).
+ *
+ * What the library computes (the hot path):
+ *   thousands of independent walkers, each holding one (m,n,p:r) matrix-
+ *   multiplication scheme with coefficients in
+ *   Z_T = {-1,0,1} or Z_2, run the RandomWalk
+ *   of Algorithm 1: flips, reductions
+ *   (PAPER:233-238), expand = plus/split, sign-symmetry
+ *   normalisation, best tracking with 1% plateau acceptance
+ *   (PAPER:310-313).  Every strict rank improvement is checked against
+ *   the Brent equations by a batched device verifier.  Readings of
+ *   points the paper leaves open are R1-R23 in DESIGN.md.
+ *
+ * Conventions for every function:
+ *   - returns FG_OK (0) or a negative fg_status; nothing throws across the ABI;
+ *     on error no output buffer is partially written;
+ *   - every pointer argument is a HOST pointer owned by the caller, except where
+ *     stated; the ctx owns all device memory it allocates;
+ *   - one ctx per host thread; no callbacks; work is enqueued on the CUDA stream
+ *     given to fg_create and the call synchronises that stream before returning
+ *     unless stated otherwise;
+ *   - determinism: (seed, global walker id, step index) fully determine every
+ *     trajectory (reading R8), independent of launch geometry, GPU count or how
+ *     the steps are split over fg_walk calls.
+ *
+ * Scheme interchange layout ("coeffs", SPEC:637-642 / PAPER:177-182): int8 rows,
+ * one row per rank-one term, row = [u (m*n) | v (n*p) | w (p*m)], with
+ *   u[i*n + j] = coefficient of a_ij, v[j*p + k] = coefficient of b_jk,
+ *   w[k*m + i] = coefficient of the term in c_ik (C^T order).
+ * Values in {-1,0,1} (Z_T) or {0,1} (Z_2).
+ */
+#ifndef FG_H
+#define FG_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FG_MAX_LEN  64    /* a factor has <= 64 elements (one u64 word) */
+#define FG_MAX_RCAP 512   /* rows reserved per walker (R1) */
+#define FG_NCNT     12    /* per-walker counters, see fg_get_walkers */
+
+enum fg_ring { FG_ZT = 0, FG_Z2 = 1 };
+
+enum fg_status {
+    FG_OK = 0,
+    FG_E_ARG = -1,            /* bad argument (null pointer, range, format < 1) */
+    FG_E_CAPACITY = -2,       /* mn, np or pm > 64; rank > r_cap; r_cap > 512 */
+    FG_E_DOMAIN = -3,         /* coefficient not in {-1,0,1} (Z_T) or {0,1} (Z_2); zero factor in a seed */
+    FG_E_INVALID_SCHEME = -4, /* a seed fails the Brent equations */
+    FG_E_CUDA = -5,           /* a CUDA call failed (no device, launch failure, OOM) */
+    FG_E_STATE = -6,          /* call out of order (e.g. walk before seed) */
+    FG_E_UNSUPPORTED = -7     /* format / r_cap combination without a kernel in this build */
+};
+
+/* Walk parameters (Alg. 1 inputs).  Probabilities are u32 thresholds:
+   an event with probability q fires when a Philox word x satisfies x < q*2^32
+   (reading R9).  fg_params_default() fills the defaults of DESIGN.md. */
+typedef struct fg_params {
+    uint32_t k_flip;        /* max flip draws per step, 1..16 (R11); default 16 */
+    uint32_t thr_accept_eq; /* equal-rank acceptance, "random() < 0.01": 42949672 */
+    uint32_t thr_reduce;    /* p_reduce: default 0.5 -> 2147483648 */
+    uint32_t thr_expand;    /* p_expand: default 0.01 -> 42949672 */
+    int32_t  expand_slack;  /* Alg. 1 "best_rank + 2": default 2 */
+    uint32_t phase_steps;   /* steps per kernel launch inside fg_walk (0 = all in one) */
+    uint32_t flags;         /* reserved, must be 0 */
+} fg_params;
+
+typedef struct fg_ctx fg_ctx;   /* opaque: owns the device pool and its host mirror */
+
+void fg_params_default(fg_params *out);
+const char *fg_strerror(int status);
+
+/* Create a pool of num_walkers walkers for format (m,n,p) over `ring`, each with
+   room for r_cap rows, on CUDA device `device`; work goes to `cuda_stream`
+   (a cudaStream_t; NULL = the legacy default stream).  walker_id_base is the
+   global id of local walker 0 (multi-GPU sharding); global
+   ids must stay below 2^32 (Philox counter word 2, R8).  Errors: FG_E_ARG,
+   FG_E_CAPACITY (R1), FG_E_UNSUPPORTED (no kernel variant), FG_E_CUDA. */
+int fg_create(int m, int n, int p, int ring, int r_cap, int64_t num_walkers,
+              int64_t walker_id_base, int device, void *cuda_stream, fg_ctx **out);
+void fg_destroy(fg_ctx *ctx);
+
+/* seed every walker with the naive (m,n,p : m*n*p) scheme, rows
+   ordered l = (i*n + j)*p + k; this is also each walker's initial best
+   (rank assessment).  Resets step counters, digests and counters.
+   Errors: FG_E_CAPACITY if m*n*p > r_cap. */
+int fg_seed_naive(fg_ctx *ctx);
+
+/* seed walkers [w_begin, w_end) (local indices) with one scheme of
+   `rank` rows in the interchange layout; it is verified and
+   sign-normalised on entry and duplicated over the range.  Walkers
+   outside the range are untouched.  Errors: FG_E_DOMAIN, FG_E_CAPACITY,
+   FG_E_INVALID_SCHEME, FG_E_ARG. */
+int fg_seed_pool(fg_ctx *ctx, const int8_t *coeffs, int rank, int64_t w_begin, int64_t w_end);
+
+/* Run `steps` iterations of Algorithm 1 (reading R17) on every
+   walker, Philox key = seed (R8).  Split into launches of params->phase_steps
+   steps.  After the walk: the batched verifier checks every strict improvement
+   queued by the walk (R19), and the local best (rank, naive additions, walker id)
+   is recomputed (R20, R21).  params may be NULL (defaults).  Synchronous.
+   Errors: FG_E_STATE (not seeded), FG_E_ARG, FG_E_CUDA. */
+int fg_walk(fg_ctx *ctx, uint64_t steps, uint64_t seed, const fg_params *params);
+
+/* Pure host, exact Brent check (reading R7) of one scheme in the
+   interchange layout.  Returns FG_OK if it verifies; FG_E_INVALID_SCHEME if not,
+   with the lexicographically first failing (a,b,c) in first_fail (else -1s);
+   FG_E_DOMAIN / FG_E_CAPACITY / FG_E_ARG on bad input.  Needs no GPU. */
+int fg_verify(int m, int n, int p, int ring, const int8_t *coeffs, int rank,
+              int32_t first_fail[3]);
+
+/* Batched device Brent check of `count` schemes (the walk's verifier kernel,
+   exposed): coeffs is count * r_cap rows (row-padded), ranks[k] rows used.
+   ok_out[k] = 1 if scheme k verifies, first_fail_out[3k..3k+2] as fg_verify. */
+int fg_verify_batch(fg_ctx *ctx, const int8_t *coeffs, const int32_t *ranks, int64_t count,
+                    int32_t *ok_out, int32_t *first_fail_out);
+
+/* Best scheme known to this ctx: the lexicographic minimum of (rank, naive
+   additions PAPER:656, global walker id) over the local walkers' bests and every
+   record imported with fg_import_best (R20).  coeffs_out (may be NULL) receives
+   rank rows; it must hold r_cap rows. */
+int fg_best(const fg_ctx *ctx, int *rank, int *naive_additions, int64_t *walker_id,
+            int8_t *coeffs_out);
+
+/* Bulk read of local walkers [w_begin, w_end) for parity and debugging.  Any
+   output may be NULL.  Per walker: r, best_r, digest,
+   step index, FG_NCNT counters (steps, draws, flips, flip_fail, expand_ok,
+   expand_reject, merges, zero_removed, best_copies, improvements, reduce_calls,
+   verify_fail), and r_cap rows (zero-padded) of the current and best schemes. */
+int fg_get_walkers(const fg_ctx *ctx, int64_t w_begin, int64_t w_end, int32_t *r,
+                   int32_t *best_r, uint64_t *digest, uint64_t *step, uint64_t *cnt,
+                   int8_t *rows, int8_t *best);
+
+/* Single-walker convenience form of fg_get_walkers. */
+int fg_get_walker(const fg_ctx *ctx, int64_t w, int *rank, int *best_rank, uint64_t *digest,
+                  int8_t *coeffs_out, int8_t *best_out);
+
+/* Fixed-size best records for the multi-GPU pool sync (DESIGN.md
+   section 6): header (format, ring, r_cap, rank, additions, walker id) + the best
+   scheme as 6*r_cap u64 bit planes.  All records of one job have the same size. */
+size_t fg_record_bytes(int r_cap);
+int fg_export_best(const fg_ctx *ctx, void *record);
+/* Merge `count` records (e.g. the all-gathered records of every rank) into the
+   ctx's pool best; invalid or other-format records are rejected with FG_E_ARG. */
+int fg_import_best(fg_ctx *ctx, const void *records, int count);
+/* Host-only deterministic merge (R20) of `count` records into *out. */
+int fg_record_merge(const void *records, int count, void *out);
+/* Host-only: build a record from a scheme (interchange layout). */
+int fg_record_pack(int m, int n, int p, int ring, int r_cap, const int8_t *coeffs, int rank,
+                   int64_t walker_id, void *record);
+/* Host-only: read a record back (rank, additions, walker id, coeffs r_cap rows). */
+int fg_record_unpack(const void *record, int *m, int *n, int *p, int *ring, int *rank,
+                     int *additions, int64_t *walker_id, int8_t *coeffs_out);
+
+/* Reading R23 (plateau restart, off unless called): every local walker whose
+   best rank exceeds the pool best rank + slack is re-seeded with the pool best
+   scheme (current and best); its step counter, counters continue and its digest
+   records the restart.  *restarted receives the number re-seeded. */
+int fg_restart(fg_ctx *ctx, int slack, int64_t *restarted);
+
+/* Checkpoint / resume and host-buffer I/O: the complete walker state (planes of
+   current and best schemes, ranks, step indices, digests, counters) as an opaque
+   byte image of fg_state_bytes(ctx) bytes.  Resuming from it continues every
+   trajectory bit-exactly (R8). */
+size_t fg_state_bytes(const fg_ctx *ctx);
+int fg_save_state(const fg_ctx *ctx, void *host_buf);
+int fg_load_state(fg_ctx *ctx, const void *host_buf);
+
+/* Totals since create: out[0] steps, [1] draws, [2] flips, [3] expands,
+   [4] merges + zero removals, [5] verified candidates, [6] verify failures,
+   [7] verify-queue overflows, [8] kernel launches, [9] walk kernel ms (x1000),
+   [10] verify kernel ms (x1000), [11] walk launches.  out must hold 12. */
+int fg_stats(const fg_ctx *ctx, uint64_t out[12]);
+
+/* Which kernel variant fg_walk uses for this ctx ("warp32_zt_u32k", ...). */
+const char *fg_kernel_name(const fg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -113,7 +113,9 @@ void or_local_reduce_public(or_walker *w, int a, int b);
 /* many walkers in one flat call (bench cpu baseline / tests): walker k has global
    id id_base+k, all seeded naive (or from coeffs if rank>0).  Output per walker:
    r, best_r, digest, cnt[OR_NCNT], and optionally rows/best (R*(mn+np+pm) int8). */
+/* ids (may be NULL): explicit global ids; else id_base + k */
 int  or_run_walkers(int m, int n, int p, int ring, int R, int64_t count, uint64_t id_base,
+                    const uint64_t *ids,
                     const int8_t *seed_coeffs, int seed_rank, uint64_t steps, uint64_t seed,
                     const or_params *prm, int threads,
                     int32_t *r_out, int32_t *best_r_out, uint64_t *digest_out,

@@ -87,8 +87,8 @@ class Oracle:
         lib.or_apply_expand.argtypes = [vp, i32, i32, i32, i32]
         lib.or_reduce_all_public.argtypes = [vp]
         lib.or_local_reduce_public.argtypes = [vp, i32, i32]
-        lib.or_run_walkers.argtypes = [i32, i32, i32, i32, i32, i64, u64, vp, i32, u64, u64, vp,
-                                       i32, vp, vp, vp, vp, vp, vp]
+        lib.or_run_walkers.argtypes = [i32, i32, i32, i32, i32, i64, u64, vp, vp, i32, u64, u64,
+                                       vp, i32, vp, vp, vp, vp, vp, vp]
 
     # ---- scalar helpers ----
     def word(self, seed, step, walker_id, slot):
@@ -154,7 +154,11 @@ class Oracle:
         return OracleWalker(self, m, n, p, ring, R, walker_id)
 
     def run_walkers(self, m, n, p, ring, R, count, id_base, steps, seed, params=None,
-                    threads=None, seed_coeffs=None, want_rows=True):
+                    threads=None, seed_coeffs=None, want_rows=True, ids=None):
+        """Walkers with global ids id_base..id_base+count-1 (or the explicit ids)."""
+        if ids is not None:
+            ids = np.ascontiguousarray(ids, dtype=np.uint64)
+            count = len(ids)
         params = params or OracleParams.default()
         threads = threads or os.cpu_count() or 1
         width = m * n + n * p + p * m
@@ -165,7 +169,7 @@ class Oracle:
         rows = np.zeros((count, R, width), np.int8) if want_rows else None
         best = np.zeros((count, R, width), np.int8) if want_rows else None
         sc = None if seed_coeffs is None else np.ascontiguousarray(seed_coeffs, dtype=np.int8)
-        rc = self.lib.or_run_walkers(m, n, p, ring, R, count, id_base, _p(sc),
+        rc = self.lib.or_run_walkers(m, n, p, ring, R, count, id_base, _p(ids), _p(sc),
                                      0 if sc is None else sc.shape[0], steps, seed,
                                      C.byref(params), threads, _p(r), _p(br), _p(dg), _p(cnt),
                                      _p(rows), _p(best))

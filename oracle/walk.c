@@ -587,7 +587,7 @@ void or_reduce_all_public(or_walker *w) { reduce_all(w); }
 void or_local_reduce_public(or_walker *w, int a, int b) { local_reduce(w, a, b); }
 
 int or_run_walkers(int m, int n, int p, int ring, int R, int64_t count, uint64_t id_base,
-                   const int8_t *seed_coeffs, int seed_rank, uint64_t steps, uint64_t seed,
+                   const uint64_t *ids, const int8_t *seed_coeffs, int seed_rank, uint64_t steps, uint64_t seed,
                    const or_params *prm, int threads,
                    int32_t *r_out, int32_t *best_r_out, uint64_t *digest_out,
                    uint64_t *cnt_out, int8_t *rows_out, int8_t *best_out)
@@ -598,7 +598,7 @@ int or_run_walkers(int m, int n, int p, int ring, int R, int64_t count, uint64_t
 #pragma omp parallel for schedule(dynamic, 1) num_threads(threads) reduction(| : err)
     for (k = 0; k < count; k++) {
         or_walker w;
-        int rc = or_walker_init(&w, m, n, p, ring, R, id_base + (uint64_t)k);
+        int rc = or_walker_init(&w, m, n, p, ring, R, ids ? ids[k] : id_base + (uint64_t)k);
         if (rc == 0) rc = seed_rank > 0 ? or_seed_rows(&w, seed_coeffs, seed_rank) : or_seed_naive(&w);
         if (rc != 0) { err |= 1; or_walker_free(&w); continue; }
         or_walk(&w, steps, seed, prm);

@@ -1,0 +1,215 @@
+"""GPU (libfg.so, sm_100a) against the CPU oracle, through the C ABI.
+
+The bar: every walker trajectory is bit-exact -- final
+scheme, best scheme, ranks, step index, 12 counters and the 64-bit event digest
+that folds (rank, best, flags, touched rows, draws) of EVERY step.
+"""
+import numpy as np
+import pytest
+
+from golden_io import load_scheme
+from oracle import Oracle, OracleParams
+from paper_2511_20317_b200.inputs import WORKLOADS, perturbations, sample_walkers
+
+pytestmark = pytest.mark.gpu
+ZT, Z2 = 0, 1
+
+
+@pytest.fixture(scope="module")
+def fg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_20317_b200 import fg as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+def _stream():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ctx(fg, m, n, p, ring, R, W, base=0):
+    return fg.FlipGraph(m, n, p, ring, R, W, base, 0, _stream())
+
+
+def _oparams(fp):
+    return OracleParams.default(k_flip=fp.k_flip, thr_accept_eq=fp.thr_accept_eq,
+                                thr_reduce=fp.thr_reduce, thr_expand=fp.thr_expand,
+                                expand_slack=fp.expand_slack)
+
+
+def _assert_same(got, ref, idx=None, what=""):
+    for k in ("r", "best_r", "digest", "cnt", "rows", "best"):
+        g = got[k] if idx is None else got[k][idx]
+        if not np.array_equal(g, ref[k]):
+            bad = np.nonzero(np.any((g != ref[k]).reshape(len(g), -1), axis=1))[0]
+            raise AssertionError(f"{what}: {k} differs for walkers {bad[:10]} "
+                                 f"(gpu {g[bad[0]] if k in ('r','best_r','digest') else ''} "
+                                 f"oracle {ref[k][bad[0]] if k in ('r','best_r','digest') else ''})")
+
+
+@pytest.mark.parametrize("ring", [ZT, Z2])
+def test_c1_all_64_walkers_to_strassen(fg, orc, ring):
+    """Config C1: (2,2,2) naive -> 7, all 64 trajectories bit-exact."""
+    wl = WORKLOADS["c1_222_zt"]
+    steps = 60000
+    g = _ctx(fg, 2, 2, 2, ring, wl.r_cap, 64)
+    g.seed_naive()
+    g.walk(steps, wl.seed + ring)
+    got = g.get_walkers()
+    ref = orc.run_walkers(2, 2, 2, ring, wl.r_cap, 64, 0, steps, wl.seed + ring)
+    _assert_same(got, ref, what="c1")
+    assert np.all(got["best_r"] == 7)
+    assert np.all(got["step"] == steps)
+    st = g.stats()
+    assert st["verify_fail"] == 0 and st["queue_overflow"] == 0
+    assert st["verified"] == int(got["cnt"][:, 9].sum())
+    b = g.best()
+    assert b["rank"] == 7 and fg.fg_verify(2, 2, 2, ring, b["coeffs"])[0] == 0
+
+
+@pytest.mark.parametrize("ring", [ZT, Z2])
+def test_c2_sampled_walkers(fg, orc, ring):
+    """Config C2: (3,3,3) with 16384 walkers at full size; 96 sampled trajectories
+    bit-exact against the oracle; every walker's scheme verifies on the device."""
+    wl = WORKLOADS["c2_333_zt"]
+    steps = 3000
+    W = wl.walkers
+    g = _ctx(fg, 3, 3, 3, ring, wl.r_cap, W)
+    g.seed_naive()
+    g.walk(steps, wl.seed + ring)
+    got = g.get_walkers()
+    ids = sample_walkers(W, 96, seed=ring)
+    ref = orc.run_walkers(3, 3, 3, ring, wl.r_cap, 0, 0, steps, wl.seed + ring, ids=ids)
+    _assert_same(got, ref, idx=ids, what="c2")
+    st = g.stats()
+    assert st["verify_fail"] == 0 and st["queue_overflow"] == 0
+    # property at full size: every current scheme satisfies the Brent equations
+    cur = [got["rows"][k][: got["r"][k]] for k in range(0, W, 7)]
+    ok, _ = g.verify_batch(cur)
+    assert np.all(ok == 1)
+    assert np.all(got["r"] <= wl.r_cap) and np.all(got["best_r"] <= 27)
+
+
+def test_phase_split_and_params(fg, orc):
+    """Counter-based RNG: one call of 2400 steps == calls of 1000+900+500 with
+    phase_steps 333 inside; non-default parameters are honoured identically."""
+    p = fg.params_default(k_flip=4, thr_reduce=1 << 30, thr_expand=1 << 28, expand_slack=1)
+    a = _ctx(fg, 3, 3, 3, ZT, 32, 256, base=1000)
+    b = _ctx(fg, 3, 3, 3, ZT, 32, 256, base=1000)
+    a.seed_naive()
+    b.seed_naive()
+    a.walk(2400, 77, p)
+    p.phase_steps = 333
+    for s in (1000, 900, 500):
+        b.walk(s, 77, p)
+    ga, gb = a.get_walkers(), b.get_walkers()
+    _assert_same(ga, gb, what="split")
+    ids = sample_walkers(256, 24, seed=3)
+    ref = orc.run_walkers(3, 3, 3, ZT, 32, 0, 0, 2400, 77, params=_oparams(p), ids=ids + 1000)
+    _assert_same(ga, ref, idx=ids, what="params")
+
+
+def test_edge_formats(fg, orc):
+    """Degenerate and ragged cases: (1,1,1:1) (no flip, no expand), capacity
+    R = naive rank (every expand rejected), non-square (2,3,4), Strassen seed
+    (no candidates: expand fallback), R below 32 and a ragged walker count."""
+    cases = [((1, 1, 1), ZT, 4, 37, None), ((2, 2, 2), ZT, 8, 33, None),
+             ((2, 3, 4), ZT, 32, 70, None), ((2, 3, 4), Z2, 32, 70, None),
+             ((2, 2, 2), ZT, 12, 40, "sec36_after.txt"), ((3, 2, 3), ZT, 30, 65, None),
+             ((2, 4, 2), ZT, 32, 31, None)]
+    for (m, n, p), ring, R, W, seedfile in cases:
+        g = _ctx(fg, m, n, p, ring, R, W, base=5)
+        seedc = None
+        if seedfile:
+            _, _, _, seedc = load_scheme(seedfile)
+            g.seed_pool(seedc)
+        else:
+            g.seed_naive()
+        g.walk(1500, 4242)
+        got = g.get_walkers()
+        ref = orc.run_walkers(m, n, p, ring, R, W, 5, 1500, 4242, seed_coeffs=seedc)
+        _assert_same(got, ref, what=f"{(m, n, p)} ring {ring} R {R}")
+
+
+def test_zero_steps_and_best(fg, orc):
+    g = _ctx(fg, 3, 3, 3, ZT, 32, 50)
+    g.seed_naive()
+    g.walk(0, 1)
+    b = g.best()
+    assert b["rank"] == 27 and b["walker_id"] == 0
+    assert b["additions"] == orc.additions(3, 3, 3, orc.naive(3, 3, 3))
+
+
+def test_verify_batch_matches_oracle(fg, orc):
+    rng = np.random.default_rng(11)
+    g = _ctx(fg, 3, 3, 3, ZT, 32, 64)
+    g.seed_naive()
+    g.walk(4000, 9)
+    got = g.get_walkers()
+    schemes = [got["best"][k][: got["best_r"][k]] for k in range(64)]
+    for (l, e, v) in perturbations(20, 27, ZT, 60, seed=1):
+        k = int(rng.integers(64))
+        c = schemes[k].copy()
+        c[l % len(c), e] = v
+        schemes.append(c)
+    ok, ff = g.verify_batch(schemes)
+    for k, c in enumerate(schemes):
+        rc, off = orc.verify(3, 3, 3, ZT, c)
+        assert ok[k] == (1 if rc == 0 else 0)
+        assert tuple(ff[k]) == off
+    # Z2
+    g2 = _ctx(fg, 2, 3, 4, Z2, 32, 4)
+    base = orc.naive(2, 3, 4)
+    sch = [base]
+    for (l, e, v) in perturbations(24, base.shape[1], Z2, 30, seed=2):
+        c = base.copy()
+        c[l, e] = v
+        sch.append(c)
+    ok, ff = g2.verify_batch(sch)
+    for k, c in enumerate(sch):
+        rc, off = orc.verify(2, 3, 4, Z2, c)
+        assert ok[k] == (1 if rc == 0 else 0) and tuple(ff[k]) == off
+
+
+def test_state_roundtrip_resumes_exactly(fg):
+    a = _ctx(fg, 3, 3, 3, ZT, 32, 128)
+    a.seed_naive()
+    a.walk(700, 5)
+    img = a.save_state()
+    a.walk(800, 5)
+    b = _ctx(fg, 3, 3, 3, ZT, 32, 128)
+    b.load_state(img)
+    b.walk(800, 5)
+    _assert_same(a.get_walkers(), b.get_walkers(), what="resume")
+
+
+def test_restart_matches_oracle(fg, orc):
+    """R23: walkers whose best is worse than pool best + slack are re-seeded."""
+    m, n, p, strassen = load_scheme("sec36_after.txt")
+    g = _ctx(fg, 2, 2, 2, ZT, 32, 40)
+    g.seed_naive()
+    g.walk(200, 3)
+    rec = fg.fg_record_pack(2, 2, 2, ZT, 32, strassen, 999)
+    g.import_best(rec, 1)
+    pool = g.best()                      # the scheme restart will use (R20 minimum)
+    before = g.get_walkers()
+    n = g.restart(0)
+    assert n == int(np.sum(before["best_r"] > pool["rank"]))
+    g.walk(300, 3)
+    got = g.get_walkers()
+    for k in range(40):
+        w = orc.walker(2, 2, 2, ZT, 32, walker_id=k)
+        w.seed_naive()
+        w.walk(200, 3)
+        if w.best_r > pool["rank"]:
+            w.restart(pool["coeffs"])
+        w.walk(300, 3)
+        assert w.digest == got["digest"][k] and w.r == got["r"][k]
+        assert np.array_equal(w.rows(), got["rows"][k][: w.r])
