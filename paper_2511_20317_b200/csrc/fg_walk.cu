@@ -1,19 +1,24 @@
 // fg_walk.cu -- the RandomWalk kernel (Algorithm 1) for walkers
 // with at most 32 rows: ONE WALKER PER WARP, row l of the scheme in lane l's
-// registers, every step's control flow warp-uniform.
+// registers, every step's control flow warp-uniform and (on the hot path)
+// branch-free.
 //
 // Per step (reading R17):
-//   - Philox words: lane L precomputes blocks 0 and 2 of step s0+L for 32 steps,
-//     fetched with SHFL; blocks 1 and 3-5 on demand (R8).
-//   - flip candidates (R10): MATCH.ANY over the packed (digits, signs) key of each
-//     role gives each lane the set of rows sharing its factor; |C| and the k-th
-//     candidate come from popc + one warp prefix scan + a ballot (no O(r^2) list).
-//   - try_flip (R11): two SHFLs exchange the factors, LOP3 ternary add/sub with
-//     the fused validity vote, per-lane sign normalisation.
-//   - local reduction check (R12): refreshed match masks; the exact (rare) worklist
-//     path runs only if a touched row has a zero factor or shares two factors.
-//   - acceptance, reduce_all (R15, exact skip via the masks),
-//     expand (R16) with row broadcasts.
+//   - Philox words (R8): lane L computes blocks 0 and 2 of step s0+L once per 32
+//     steps into a per-warp shared-memory table; a step reads its words with LDS.
+//   - flip candidates (R10): each lane keeps the masks of rows equal to its u, its
+//     v and its w up to sign (mU, mV, mWp); |C| and the prefix over (role, i) come
+//     from popc + one packed warp scan.
+//   - try_flip (R11): the first five draws are evaluated LANE-PARALLEL (lane a =
+//     draw a: binary search of the prefix, nth-set-bit for j, row fetch by SHFL,
+//     LOP3 ternary add/sub with validity); a ballot picks the first valid draw,
+//     exactly the draw the sequential loop would commit.  Draws 5..15 (rare) run
+//     the same way from on-demand Philox blocks 3-5.
+//   - the masks are then updated for the two touched rows only (SHFL + compare +
+//     ballot); MATCH.ANY (10x the cost of SHFL on sm_100, tools/microbench) is
+//     used only after the rare structural changes (merges, removals, expand).
+//   - local reduction check (R12), acceptance, reduce_all (R15,
+//     exact skip through the masks), expand (R16).
 // Independent of oracle/; parity is checked by tests/test_gpu_parity.py.
 #include <cstdio>
 #include "fg_device.cuh"
@@ -21,34 +26,55 @@
 using namespace fgd;
 
 #define W32_THREADS 128
+#define W32_WARPS (W32_THREADS / 32)
+#define PXS 9                        // words per step in the Philox table (8 + 1 pad)
 
 namespace {
 
-template <int RING, typename T, bool K16>
-__global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
+// position of the t-th (0-based) set bit of x; x has more than t set bits
+__device__ __forceinline__ int nth_bit(uint32_t x, uint32_t t)
 {
+    int pos = 0;
+    uint32_t c = __popc(x & 0xffffu);
+    if (t >= c) { t -= c; x >>= 16; pos += 16; }
+    c = __popc(x & 0xffu);
+    if (t >= c) { t -= c; x >>= 8; pos += 8; }
+    c = __popc(x & 0xfu);
+    if (t >= c) { t -= c; x >>= 4; pos += 4; }
+    c = __popc(x & 0x3u);
+    if (t >= c) { t -= c; x >>= 2; pos += 2; }
+    c = x & 1u;
+    if (t >= c) pos += 1;
+    return pos;
+}
+
+template <int RING, bool K16>
+__global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
+{
+    using T = uint32_t;
+    __shared__ uint32_t px_all[W32_WARPS][32 * PXS];
+    __shared__ uint32_t rc_all[W32_WARPS][8];     // rare counters (lane 0 updates)
+    uint32_t *px = px_all[threadIdx.x >> 5];
+    uint32_t *rc = rc_all[threadIdx.x >> 5];
     const int lane = threadIdx.x & 31;
     const unsigned lanebit = 1u << lane;
     const unsigned above = ~((lanebit << 1) - 1u);          // lanes > this one
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int R = a.R;
     const uint64_t seed = a.seed;
+    const uint32_t kf = a.k_flip;
 
     for (int64_t wk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wk < a.num_walkers;
          wk += nwarps) {
         // ---------------- load walker (coalesced: plane q of rows 0..31) ----------------
         const uint64_t *cp = a.cur + (size_t)wk * FG_PLANES * R;
-        const uint64_t *bp = a.best + (size_t)wk * FG_PLANES * R;
-        Row<T> row, brow;
+        uint64_t *bw = a.best + (size_t)wk * FG_PLANES * R;
+        Row<T> row;
         row.u.d = row.u.s = row.v.d = row.v.s = row.w.d = row.w.s = 0;
-        brow = row;
         if (lane < R) {
             row.u.d = (T)cp[0 * R + lane]; row.u.s = (T)cp[1 * R + lane];
             row.v.d = (T)cp[2 * R + lane]; row.v.s = (T)cp[3 * R + lane];
             row.w.d = (T)cp[4 * R + lane]; row.w.s = (T)cp[5 * R + lane];
-            brow.u.d = (T)bp[0 * R + lane]; brow.u.s = (T)bp[1 * R + lane];
-            brow.v.d = (T)bp[2 * R + lane]; brow.v.s = (T)bp[3 * R + lane];
-            brow.w.d = (T)bp[4 * R + lane]; brow.w.s = (T)bp[5 * R + lane];
         }
         fg_whdr *hp = a.hdr + wk;
         int r = hp->r;
@@ -57,26 +83,43 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
         uint64_t digest = hp->digest;
         const uint32_t wid = (uint32_t)(a.id_base + wk);
 
-        uint32_t c_draws = 0, c_flips = 0, c_eok = 0, c_erej = 0, c_merge = 0, c_zero = 0,
-                 c_copy = 0, c_impr = 0, c_red = 0;
+        uint32_t c_draws = 0, c_flips = 0, c_red = 0;
+        if (lane < 8) rc[lane] = 0;
+        __syncwarp();
+        enum { RC_EOK = 0, RC_EREJ, RC_MERGE, RC_ZERO, RC_COPY, RC_IMPR };
+        auto bump = [&](int k, uint32_t v) { if (lane == 0) rc[k] += v; };
 
-        unsigned mU = 0, mV = 0, mW = 0, mWp = 0;
-        bool masks_ok = false;
+        // masks of live lanes holding the same u / v / w-up-to-sign as this lane
+        unsigned mU = 0, mV = 0, mWp = 0;
+        auto wabs = [&](Tv<T> w) {
+            const T nw = (w.s & (w.d & (T)(0 - w.d))) ? ~(T)0 : (T)0;
+            w.s ^= w.d & nw;
+            return w;
+        };
         auto compute_masks = [&]() {
             const unsigned act = r >= 32 ? FULL : ((1u << r) - 1u);
             mU = match<RING, T, K16>(row.u) & act;
             mV = match<RING, T, K16>(row.v) & act;
-            mW = match<RING, T, K16>(row.w) & act;
-            if (RING == FG_ZT) {
-                // W up to sign: key of the sign-normalised w
-                Tv<T> wa = row.w;
-                const T nw = (wa.s & (wa.d & (T)(0 - wa.d))) ? ~(T)0 : (T)0;
-                wa.s ^= wa.d & nw;
-                mWp = match<RING, T, K16>(wa) & act;
-            } else {
-                mWp = mW;
-            }
-            masks_ok = true;
+            mWp = (RING == FG_ZT ? match<RING, T, K16>(wabs(row.w)) : match<RING, T, K16>(row.w)) & act;
+        };
+        // incremental update after rows ta != tb changed (all other rows unchanged)
+        auto update_masks2 = [&](int ta, int tb) {
+            const Row<T> ra = shfl_row<RING, T, K16>(row, ta);
+            const Row<T> rb = shfl_row<RING, T, K16>(row, tb);
+            const bool live = lane < r;
+            const Tv<T> aw = wabs(row.w);
+            const bool ua = live && eq(row.u, ra.u), ub = live && eq(row.u, rb.u);
+            const bool va = live && eq(row.v, ra.v), vb = live && eq(row.v, rb.v);
+            const bool wa_ = live && eq(aw, wabs(ra.w)), wb_ = live && eq(aw, wabs(rb.w));
+            const unsigned keep = ~((1u << ta) | (1u << tb));
+            mU = (mU & keep) | ((unsigned)ua << ta) | ((unsigned)ub << tb);
+            mV = (mV & keep) | ((unsigned)va << ta) | ((unsigned)vb << tb);
+            mWp = (mWp & keep) | ((unsigned)wa_ << ta) | ((unsigned)wb_ << tb);
+            const unsigned bua = __ballot_sync(FULL, ua), bub = __ballot_sync(FULL, ub);
+            const unsigned bva = __ballot_sync(FULL, va), bvb = __ballot_sync(FULL, vb);
+            const unsigned bwa = __ballot_sync(FULL, wa_), bwb = __ballot_sync(FULL, wb_);
+            if (lane == ta) { mU = bua; mV = bva; mWp = bwa; }
+            if (lane == tb) { mU = bub; mV = bvb; mWp = bwb; }
         };
 
         // R14 remove(h) with the 2-entry worklist (entries == h dropped, r-1 -> h)
@@ -106,7 +149,7 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                 const Row<T> rt = shfl_row<RING, T, K16>(row, t);
                 if (has_zero(rt)) {
                     remove_row(t, wl0, wl1, nwl);
-                    c_zero++;
+                    bump(RC_ZERO, 1);
                     continue;
                 }
                 Row<T> merged = row;
@@ -117,11 +160,11 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                 const int lo = t < j ? t : j, hi = t < j ? j : t;
                 const Row<T> mg = shfl_row<RING, T, K16>(merged, j);
                 if (lane == lo) row = mg;
-                c_merge++;
+                bump(RC_MERGE, 1);
                 remove_row(hi, wl0, wl1, nwl);
                 if (has_zero(mg)) {
                     remove_row(lo, wl0, wl1, nwl);
-                    c_zero++;
+                    bump(RC_ZERO, 1);
                 } else {
                     wl1 = wl0;
                     wl0 = lo;
@@ -137,7 +180,7 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                 if (bz) {
                     int n0 = 0, x0 = 0, x1 = 0;
                     remove_row(__ffs(bz) - 1, x0, x1, n0);
-                    c_zero++;
+                    bump(RC_ZERO, 1);
                     continue;
                 }
                 compute_masks();
@@ -155,12 +198,12 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                     const int j = __ffs(bal) - 1;
                     const Row<T> mg = shfl_row<RING, T, K16>(merged, j);
                     if (lane == i) row = mg;
-                    c_merge++;
+                    bump(RC_MERGE, 1);
                     int n0 = 0, x0 = 0, x1 = 0;
                     remove_row(j, x0, x1, n0);
                     if (has_zero(mg)) {
                         remove_row(i, x0, x1, n0);
-                        c_zero++;
+                        bump(RC_ZERO, 1);
                     }
                     merged_any = true;
                     break;
@@ -183,12 +226,12 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
             const int A = perm >> 1;
             const int B = (1161 >> (2 * perm)) & 3;
             const int Cr = 3 - A - B;
-            const Tv<T> fa = get(row, A), fb = get(row, B), fc = get(row, Cr);
-            const Tv<T> ai = shfl<T, K16>(fa, i), aj = shfl<T, K16>(fa, j);
+            const Row<T> ri = shfl_row<RING, T, K16>(row, i);
+            const Row<T> rj = shfl_row<RING, T, K16>(row, j);
+            const Tv<T> ai = get(ri, A), aj = get(rj, A), bi = get(ri, B), bj = get(rj, B);
+            const Tv<T> ci = get(ri, Cr), cj = get(rj, Cr);
             bool ok = true;
             if (plus) {
-                const Tv<T> bi = shfl<T, K16>(fb, i), bj = shfl<T, K16>(fb, j);
-                const Tv<T> ci = shfl<T, K16>(fc, i), cj = shfl<T, K16>(fc, j);
                 if (!distinct<RING, T>(ai, aj) || !distinct<RING, T>(bi, bj) ||
                     !distinct<RING, T>(ci, cj))
                     return false;
@@ -204,7 +247,6 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                 set(row, Cr, cj, lane == r);
             } else {
                 if (!distinct<RING, T>(ai, aj)) return false;
-                const Tv<T> bi = shfl<T, K16>(fb, i), ci = shfl<T, K16>(fc, i);
                 const Tv<T> t3 = sub<RING, T>(ai, aj, ok);      // u_i - u_j
                 if (!ok) return false;
                 set(row, A, aj, lane == i);
@@ -214,21 +256,28 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
             }
             if (lane == i || lane == j || lane == r) normalize<RING, T>(row);
             r++;
-            masks_ok = false;
+            compute_masks();
             return true;
         };
 
-        uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0, q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+        compute_masks();
         int boff = 32;
 
-        for (uint64_t it = 0; it < a.steps; ++it, ++step, ++boff) {
+        const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
+        for (uint32_t it = 0; it < nsteps; ++it, ++step, ++boff) {
             if (boff == 32) {
-                // lane L: Philox blocks 0 and 2 of step (step + L)
-                philox_block(seed, step + lane, wid, 0u, p0, p1, p2, p3);
-                philox_block(seed, step + lane, wid, 2u, q0, q1, q2, q3);
+                // lane L: Philox blocks 0 and 2 of step (step + L) -> px[L*9 + 0..7]
+                uint32_t o0, o1, o2, o3;
+                philox_block(seed, step + lane, wid, 0u, o0, o1, o2, o3);
+                px[lane * PXS + 0] = o0; px[lane * PXS + 1] = o1;
+                px[lane * PXS + 2] = o2; px[lane * PXS + 3] = o3;
+                philox_block(seed, step + lane, wid, 2u, o0, o1, o2, o3);
+                px[lane * PXS + 4] = o0; px[lane * PXS + 5] = o1;
+                px[lane * PXS + 6] = o2; px[lane * PXS + 7] = o3;
+                __syncwarp();
                 boff = 0;
             }
-            if (!masks_ok) compute_masks();
+            const uint32_t *pw = px + boff * PXS;     // [attempt0, accept, reduce, expand_p, attempts 1..4]
             uint32_t flags = 0;
             int alpha = 0, beta = 0, draws = 0;
             bool ok = false;
@@ -248,67 +297,79 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
             const unsigned tot = __shfl_sync(FULL, incl, 31);
             const unsigned nU = tot & 1023u, nV = (tot >> 10) & 1023u, nW = tot >> 20;
             const unsigned nC = nU + nV + nW;
+            const unsigned excl = incl - cnt;
 
-            // ---- R11 try_flip ----
+            // ---- R11 try_flip: draw `att` evaluated by this lane with word x ----
+            int e_al = 0, e_be = 0, e_Y = 0, e_Z = 0;
+            Tv<T> e_ny, e_nz;
+            auto eval = [&](uint32_t x) -> bool {
+                const uint32_t k = __umulhi(x, 4u * nC);
+                const uint32_t idx = k >> 2;
+                const int d = k & 1, e = (k >> 1) & 1;
+                const int X = idx < nU ? 0 : (idx < nU + nV ? 1 : 2);
+                const uint32_t qq = idx - (X == 0 ? 0u : (X == 1 ? nU : nU + nV));
+                const int sh = 10 * X;
+                int i = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const unsigned v = (__shfl_sync(FULL, incl, i + st - 1) >> sh) & 1023u;
+                    i += (v <= qq) ? st : 0;
+                }
+                const unsigned ex_i = (__shfl_sync(FULL, excl, i) >> sh) & 1023u;
+                const unsigned mu_i = __shfl_sync(FULL, mU, i);
+                const unsigned mv_i = __shfl_sync(FULL, mV, i);
+                const unsigned mw_i = __shfl_sync(FULL, mWp, i);
+                const unsigned mm = (X == 0 ? mu_i : (X == 1 ? mv_i : mw_i)) & ~((2u << i) - 1u);
+                const int j = nth_bit(mm, qq - ex_i);
+                const int al = d ? j : i, be = d ? i : j;
+                int Y, Z;
+                if (X == 0) { Y = 1; Z = 2; } else if (X == 1) { Y = 2; Z = 0; } else { Y = 0; Z = 1; }
+                if (e) { const int tt = Y; Y = Z; Z = tt; }
+                const Row<T> ra = shfl_row<RING, T, K16>(row, al);
+                const Row<T> rb = shfl_row<RING, T, K16>(row, be);
+                // sigma = -1 iff the shared factor is W and the two are negatives
+                const bool sneg = RING == FG_ZT && X == 2 && !eq(ra.w, rb.w);
+                bool v = true;
+                const Tv<T> yb = get(rb, Y);
+                e_ny = add<RING, T>(get(ra, Y), sneg ? neg(yb) : yb, v);     // y_a + s y_b
+                e_nz = sub<RING, T>(get(rb, Z), get(ra, Z), v);              // z_b - z_a
+                e_al = al; e_be = be; e_Y = Y; e_Z = Z;
+                return v;
+            };
+
             if (nC) {
-                uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;   // blocks 3..5 on demand
-                const uint32_t kf = a.k_flip;
-                for (uint32_t at = 0; at < kf; ++at) {
-                    uint32_t x;
-                    if (at == 0) {
-                        x = __shfl_sync(FULL, p0, boff);
-                    } else if (at <= 4) {
-                        const uint32_t qs = at == 1 ? q0 : (at == 2 ? q1 : (at == 3 ? q2 : q3));
-                        x = __shfl_sync(FULL, qs, boff);
-                    } else {
-                        const uint32_t slot = 7 + at;
-                        if ((slot & 3) == 0 || at == 5)
-                            philox_block(seed, step, wid, slot >> 2, e0, e1, e2, e3);
-                        const uint32_t wsel = slot & 3;
-                        x = wsel == 0 ? e0 : (wsel == 1 ? e1 : (wsel == 2 ? e2 : e3));
-                    }
-                    draws++;
-                    const uint32_t k = __umulhi(x, 4u * nC);
-                    const uint32_t idx = k >> 2;
-                    const int d = k & 1, e = (k >> 1) & 1;
-                    int X;
-                    uint32_t qq;
-                    if (idx < nU) { X = 0; qq = idx; }
-                    else if (idx < nU + nV) { X = 1; qq = idx - nU; }
-                    else { X = 2; qq = idx - nU - nV; }
-                    const int sh = 10 * X;
-                    const unsigned inX = (incl >> sh) & 1023u;
-                    const int i = __ffs(__ballot_sync(FULL, inX > qq)) - 1;
-                    unsigned info = 0;
-                    if (lane == i) {
-                        unsigned t = qq - (inX - ((cnt >> sh) & 1023u));
-                        unsigned mm = (X == 0 ? mU : (X == 1 ? mV : mWp)) & above;
-                        for (; t; --t) mm &= mm - 1u;
-                        const int j = __ffs(mm) - 1;
-                        const unsigned ng = (RING == FG_ZT && X == 2) ? (((mW >> j) & 1u) ^ 1u) : 0u;
-                        info = (unsigned)j | (ng << 8);
-                    }
-                    info = __shfl_sync(FULL, info, i);
-                    const int j = info & 255;
-                    const bool sneg = (info >> 8) != 0;
-                    const int al = d ? j : i, be = d ? i : j;
-                    int Y, Z;
-                    if (X == 0) { Y = 1; Z = 2; } else if (X == 1) { Y = 2; Z = 0; } else { Y = 0; Z = 1; }
-                    if (e) { const int tt = Y; Y = Z; Z = tt; }
-                    const Tv<T> fy = get(row, Y), fz = get(row, Z);
-                    const Tv<T> recv = shfl<T, K16>(lane == be ? fy : fz, lane == al ? be : al);
-                    bool va = true, vb = true;
-                    const Tv<T> ny = add<RING, T>(fy, sneg ? neg(recv) : recv, va);  // y_a + s y_b
-                    const Tv<T> nz = sub<RING, T>(fz, recv, vb);                      // z_b - z_a
-                    const bool bad = (lane == al && !va) || (lane == be && !vb);
-                    if (__any_sync(FULL, bad)) continue;
-                    set(row, Y, ny, lane == al);
-                    set(row, Z, nz, lane == be);
-                    if (lane == al || lane == be) normalize<RING, T>(row);
-                    alpha = al;
-                    beta = be;
+                // draws 0..4: lane a evaluates draw a (words: block 0 word 0, block 2 words 0..3)
+                const int na = kf < 5 ? (int)kf : 5;
+                const uint32_t x = pw[lane == 0 ? 0 : (lane < 5 ? 3 + lane : 0)];
+                unsigned win = __ballot_sync(FULL, eval(x) && lane < na);
+                int base = 0;
+                if (!win && kf > 5) {
+                    // draws 5..15: slots 12..22 = Philox blocks 3,4,5 of this step
+                    uint32_t o0, o1, o2, o3;
+                    philox_block(seed, step, wid, 3u + (lane < 3 ? lane : 0), o0, o1, o2, o3);
+                    const int att = 5 + lane;                       // slot 7 + att
+                    const int src = (att + 7 - 12) >> 2, w = (att + 7) & 3;
+                    const uint32_t w0 = __shfl_sync(FULL, o0, src & 3), w1 = __shfl_sync(FULL, o1, src & 3);
+                    const uint32_t w2 = __shfl_sync(FULL, o2, src & 3), w3 = __shfl_sync(FULL, o3, src & 3);
+                    const uint32_t xb = w == 0 ? w0 : (w == 1 ? w1 : (w == 2 ? w2 : w3));
+                    win = __ballot_sync(FULL, eval(xb) && att < (int)kf);
+                    base = 5;
+                    draws = 5;
+                }
+                if (win) {
+                    const int src = __ffs(win) - 1;
+                    draws = base + src + 1;
+                    const unsigned info = __shfl_sync(FULL, (unsigned)(e_al | (e_be << 8) | (e_Y << 16) | (e_Z << 18)), src);
+                    const Tv<T> ny = shfl<T, K16>(e_ny, src);
+                    const Tv<T> nz = shfl<T, K16>(e_nz, src);
+                    alpha = info & 255;
+                    beta = (info >> 8) & 255;
+                    set(row, (info >> 16) & 3, ny, lane == alpha);
+                    set(row, (info >> 18) & 3, nz, lane == beta);
+                    if (lane == alpha || lane == beta) normalize<RING, T>(row);
                     ok = true;
-                    break;
+                } else {
+                    draws = kf;
                 }
             }
             c_draws += draws;
@@ -316,13 +377,13 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
             if (!ok) {
                 // expand; continue
                 const bool ex = expand();
-                c_eok += ex;
-                c_erej += !ex;
+                bump(RC_EOK, ex);
+                bump(RC_EREJ, !ex);
                 flags |= 2u | (ex ? 64u : 0u);
             } else {
                 c_flips++;
                 flags |= 1u;
-                compute_masks();
+                update_masks2(alpha, beta);
                 // ---- R12 local reduction (exact skip) ----
                 {
                     const unsigned two = ((mU & mV) | (mU & mWp) | (mV & mWp)) & ~lanebit;
@@ -334,16 +395,24 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                 }
                 // ---- PAPER:310-313 acceptance ----
                 bool acc = r < best;
-                if (!acc && r == best) acc = __shfl_sync(FULL, p1, boff) < a.thr_eq;
+                if (!acc && r == best) acc = pw[1] < a.thr_eq;
                 if (acc) {
                     const bool strict = r < best;
                     best = r;
-                    brow = row;
-                    c_copy++;
+                    bump(RC_COPY, 1);
                     flags |= 4u;
+                    if (lane < R) {
+                        const bool lv = lane < r;
+                        bw[0 * R + lane] = lv ? (uint64_t)row.u.d : 0;
+                        bw[1 * R + lane] = lv ? (uint64_t)row.u.s : 0;
+                        bw[2 * R + lane] = lv ? (uint64_t)row.v.d : 0;
+                        bw[3 * R + lane] = lv ? (uint64_t)row.v.s : 0;
+                        bw[4 * R + lane] = lv ? (uint64_t)row.w.d : 0;
+                        bw[5 * R + lane] = lv ? (uint64_t)row.w.s : 0;
+                    }
                     if (strict) {
                         flags |= 8u;
-                        c_impr++;
+                        bump(RC_IMPR, 1);
                         // R19: enqueue for the batched Brent verifier
                         unsigned slot = 0;
                         if (lane == 0) slot = atomicAdd(a.q_count, 1u);
@@ -371,7 +440,7 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                     }
                 }
                 // ---- PAPER:315-317 reduce (R15) ----
-                if (__shfl_sync(FULL, p2, boff) < a.thr_reduce) {
+                if (pw[2] < a.thr_reduce) {
                     c_red++;
                     flags |= 16u;
                     const unsigned two = ((mU & mV) | (mU & mWp) | (mV & mWp)) & ~lanebit;
@@ -381,11 +450,11 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                     }
                 }
                 // ---- PAPER:319-321 expand ----
-                if (__shfl_sync(FULL, p3, boff) < a.thr_expand && r <= best + a.slack) {
+                if (pw[3] < a.thr_expand && r <= best + a.slack) {
                     const bool ex = expand();
                     flags |= 32u | (ex ? 64u : 0u);
-                    c_eok += ex;
-                    c_erej += !ex;
+                    bump(RC_EOK, ex);
+                    bump(RC_EREJ, !ex);
                 }
             }
             // ---- digest ----
@@ -394,22 +463,20 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                                 ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
             digest = (digest ^ ev) * 0x100000001b3ULL;
             digest ^= digest >> 32;
+            __syncwarp();
         }
 
         // ---------------- store walker ----------------
         uint64_t *cw = a.cur + (size_t)wk * FG_PLANES * R;
-        uint64_t *bw = a.best + (size_t)wk * FG_PLANES * R;
         if (lane < R) {
             cw[0 * R + lane] = (uint64_t)row.u.d; cw[1 * R + lane] = (uint64_t)row.u.s;
             cw[2 * R + lane] = (uint64_t)row.v.d; cw[3 * R + lane] = (uint64_t)row.v.s;
             cw[4 * R + lane] = (uint64_t)row.w.d; cw[5 * R + lane] = (uint64_t)row.w.s;
-            bw[0 * R + lane] = (uint64_t)brow.u.d; bw[1 * R + lane] = (uint64_t)brow.u.s;
-            bw[2 * R + lane] = (uint64_t)brow.v.d; bw[3 * R + lane] = (uint64_t)brow.v.s;
-            bw[4 * R + lane] = (uint64_t)brow.w.d; bw[5 * R + lane] = (uint64_t)brow.w.s;
         }
-        // naive additions of the best -> local best key (R20)
-        const int nnz = lane < best ? (__popcll((uint64_t)brow.u.d) + __popcll((uint64_t)brow.v.d) +
-                                       __popcll((uint64_t)brow.w.d))
+        // naive additions of the best -> local best key (R20); each lane
+        // re-reads the best row it wrote itself
+        const int nnz = lane < best ? (__popcll(bw[0 * R + lane]) + __popcll(bw[2 * R + lane]) +
+                                       __popcll(bw[4 * R + lane]))
                                     : 0;
         const int tot_nnz = __reduce_add_sync(FULL, nnz);
         if (lane == 0) {
@@ -421,12 +488,12 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
             hp->cnt[FG_CNT_DRAWS] += c_draws;
             hp->cnt[FG_CNT_FLIPS] += c_flips;
             hp->cnt[FG_CNT_FLIP_FAIL] += a.steps - c_flips;
-            hp->cnt[FG_CNT_EXPAND_OK] += c_eok;
-            hp->cnt[FG_CNT_EXPAND_REJECT] += c_erej;
-            hp->cnt[FG_CNT_MERGES] += c_merge;
-            hp->cnt[FG_CNT_ZERO_REMOVED] += c_zero;
-            hp->cnt[FG_CNT_BEST_COPIES] += c_copy;
-            hp->cnt[FG_CNT_IMPROVEMENTS] += c_impr;
+            hp->cnt[FG_CNT_EXPAND_OK] += rc[RC_EOK];
+            hp->cnt[FG_CNT_EXPAND_REJECT] += rc[RC_EREJ];
+            hp->cnt[FG_CNT_MERGES] += rc[RC_MERGE];
+            hp->cnt[FG_CNT_ZERO_REMOVED] += rc[RC_ZERO];
+            hp->cnt[FG_CNT_BEST_COPIES] += rc[RC_COPY];
+            hp->cnt[FG_CNT_IMPROVEMENTS] += rc[RC_IMPR];
             hp->cnt[FG_CNT_REDUCE_CALLS] += c_red;
             int adds = tot_nnz - 2 * best - a.mp;
             if (adds < 0) adds = 0;
@@ -435,24 +502,24 @@ __global__ void __launch_bounds__(W32_THREADS) walk_w32(WalkArgs a)
                                            (unsigned long long)wk;
             atomicMin(a.best_key, key);
         }
+        __syncwarp();
     }
 }
 
-template <int RING, typename T, bool K16>
+template <int RING, bool K16>
 cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     int bps = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_w32<RING, T, K16>,
-                                                                  W32_THREADS, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_w32<RING, K16>, W32_THREADS, 0);
     if (e != cudaSuccess) return e;
     if (bps < 1) bps = 1;
-    const int64_t wpb = W32_THREADS / 32;
+    const int64_t wpb = W32_WARPS;
     const int64_t max_warps = (int64_t)num_sms * bps * wpb;
     // even static partition: every warp runs exactly k walkers (or k-1)
     const int64_t k = (a.num_walkers + max_warps - 1) / max_warps;
     const int64_t nwarps = (a.num_walkers + k - 1) / k;
     const int64_t blocks = (nwarps + wpb - 1) / wpb;
-    walk_w32<RING, T, K16><<<(unsigned)blocks, W32_THREADS, 0, st>>>(a);
+    walk_w32<RING, K16><<<(unsigned)blocks, W32_THREADS, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -470,9 +537,9 @@ int fg_pick_kernel(int ring, int maxlen, int R)
 const char *fg_kernel_kind_name(int kind)
 {
     switch (kind) {
-    case FG_K_W32_ZT_K16: return "walk_w32<ZT,u32,key32>";
-    case FG_K_W32_ZT_K32: return "walk_w32<ZT,u32,key64>";
-    case FG_K_W32_Z2_K32: return "walk_w32<Z2,u32>";
+    case FG_K_W32_ZT_K16: return "walk_w32<ZT,key32>";
+    case FG_K_W32_ZT_K32: return "walk_w32<ZT,key64>";
+    case FG_K_W32_Z2_K32: return "walk_w32<Z2>";
     default: return "none";
     }
 }
@@ -480,9 +547,9 @@ const char *fg_kernel_kind_name(int kind)
 cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     switch (kind) {
-    case FG_K_W32_ZT_K16: return launch_w32<FG_ZT, uint32_t, true>(a, num_sms, st);
-    case FG_K_W32_ZT_K32: return launch_w32<FG_ZT, uint32_t, false>(a, num_sms, st);
-    case FG_K_W32_Z2_K32: return launch_w32<FG_Z2, uint32_t, false>(a, num_sms, st);
+    case FG_K_W32_ZT_K16: return launch_w32<FG_ZT, true>(a, num_sms, st);
+    case FG_K_W32_ZT_K32: return launch_w32<FG_ZT, false>(a, num_sms, st);
+    case FG_K_W32_Z2_K32: return launch_w32<FG_Z2, false>(a, num_sms, st);
     default: return cudaErrorInvalidValue;
     }
 }
