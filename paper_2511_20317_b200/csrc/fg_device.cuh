@@ -1,6 +1,14 @@
 // fg_device.cuh -- device primitives of the walk: bit-sliced ternary vectors
 // (PAPER:388-424), sign normalisation, Philox4x32-10 (reading R8).
 // Independent of oracle/ (no shared code).
+//
+// A factor (one of u, v, w of a rank-one term) is a ternary vector of <= 64
+// elements held as bit planes (digits = nonzero, signs = negative, signs subset of
+// digits).  Three register layouts ("policies"), chosen per format:
+//   P16  Z_T, <= 16 elements: ONE u32 key = digits | signs << 16.  Equality is one
+//        compare, a shuffle moves a whole factor, the key is the MATCH value.
+//   P32  Z_T, <= 32 elements: two u32 words (digits, signs).
+//   PZ2  Z_2, <= 32 elements: one u32 word (digits); +,- are XOR.
 #pragma once
 #include <cstdint>
 #include "fg_internal.h"
@@ -33,145 +41,167 @@ __device__ __forceinline__ void philox_block(uint64_t seed, uint64_t s, uint32_t
            o0, o1, o2, o3);
 }
 
-// ---- ternary vector: (digits, signs), signs subset of digits ----
-template <typename T> struct Tv { T d, s; };
+// ------------------------------------------------------------------------------
+// P16: key = digits | signs << 16
+struct P16 {
+    typedef uint32_t F;
+    static constexpr int RING = FG_ZT;
+    static __device__ __forceinline__ F make(uint64_t d, uint64_t s) { return (uint32_t)d | ((uint32_t)s << 16); }
+    static __device__ __forceinline__ uint64_t dig(F a) { return a & 0xffffu; }
+    static __device__ __forceinline__ uint64_t sgn(F a) { return a >> 16; }
+    static __device__ __forceinline__ bool zero(F a) { return (a & 0xffffu) == 0; }
+    static __device__ __forceinline__ bool eq(F a, F b) { return a == b; }
+    // a == -b, a != 0 (PAPER:421 with zero excluded, R4)
+    static __device__ __forceinline__ bool negeq(F a, F b)
+    {
+        const uint32_t d = a & 0xffffu;
+        return d != 0 && (a ^ b) == (d << 16);
+    }
+    static __device__ __forceinline__ F neg(F a) { return a ^ (a << 16); }
+    // first nonzero made positive (the W-up-to-sign key)
+    static __device__ __forceinline__ F abs(F a)
+    {
+        const uint32_t d = a & 0xffffu;
+        const uint32_t lb = d & (0u - d);
+        return (a & (lb << 16)) ? neg(a) : a;
+    }
+    static __device__ __forceinline__ bool first_neg(F a)
+    {
+        const uint32_t d = a & 0xffffu;
+        return (a & ((d & (0u - d)) << 16)) != 0;
+    }
+    // a + b with the ternary-safety flag (signs simplified under s subset d)
+    static __device__ __forceinline__ F add(F a, F b, bool &ok)
+    {
+        const uint32_t x = a ^ b;
+        const uint32_t d = x & 0xffffu;
+        const uint32_t s = ((a | b) >> 16) & d;
+        ok = ok && ((a & b & ~(x >> 16) & 0xffffu) == 0);
+        return __byte_perm(d, s, 0x5410);
+    }
+    static __device__ __forceinline__ F sub(F a, F b, bool &ok) { return add(a, neg(b), ok); }
+    static __device__ __forceinline__ F shfl(F a, int src) { return __shfl_sync(FULL, a, src); }
+    static __device__ __forceinline__ unsigned match(F a) { return __match_any_sync(FULL, a); }
+    static __device__ __forceinline__ F sel(bool p, F a, F b) { return p ? a : b; }
+    static __device__ __forceinline__ int popd(F a) { return __popc(a & 0xffffu); }
+};
 
-template <typename T> __device__ __forceinline__ bool eq(Tv<T> a, Tv<T> b)
-{
-    return a.d == b.d && a.s == b.s;
-}
-// a == -b, a != 0 (PAPER:421 with zero excluded, R4)
-template <typename T> __device__ __forceinline__ bool negeq(Tv<T> a, Tv<T> b)
-{
-    return a.d == b.d && a.s == (b.d ^ b.s) && a.d != 0;
-}
-template <typename T> __device__ __forceinline__ Tv<T> neg(Tv<T> a) { return {a.d, a.d ^ a.s}; }
+// P32: (digits, signs) in two words
+struct P32 {
+    struct F { uint32_t d, s; };
+    static constexpr int RING = FG_ZT;
+    static __device__ __forceinline__ F make(uint64_t d, uint64_t s) { return {(uint32_t)d, (uint32_t)s}; }
+    static __device__ __forceinline__ uint64_t dig(F a) { return a.d; }
+    static __device__ __forceinline__ uint64_t sgn(F a) { return a.s; }
+    static __device__ __forceinline__ bool zero(F a) { return a.d == 0; }
+    static __device__ __forceinline__ bool eq(F a, F b) { return a.d == b.d && a.s == b.s; }
+    static __device__ __forceinline__ bool negeq(F a, F b) { return a.d == b.d && a.s == (b.d ^ b.s) && a.d != 0; }
+    static __device__ __forceinline__ F neg(F a) { return {a.d, a.d ^ a.s}; }
+    static __device__ __forceinline__ F abs(F a) { return (a.s & (a.d & (0u - a.d))) ? neg(a) : a; }
+    static __device__ __forceinline__ bool first_neg(F a) { return (a.s & (a.d & (0u - a.d))) != 0; }
+    static __device__ __forceinline__ F add(F a, F b, bool &ok)
+    {
+        const uint32_t d = a.d ^ b.d;
+        ok = ok && ((a.d & b.d & ~(a.s ^ b.s)) == 0);
+        return {d, (a.s | b.s) & d};
+    }
+    static __device__ __forceinline__ F sub(F a, F b, bool &ok) { return add(a, neg(b), ok); }
+    static __device__ __forceinline__ F shfl(F a, int src)
+    {
+        return {__shfl_sync(FULL, a.d, src), __shfl_sync(FULL, a.s, src)};
+    }
+    static __device__ __forceinline__ unsigned match(F a)
+    {
+        return __match_any_sync(FULL, (unsigned long long)a.d | ((unsigned long long)a.s << 32));
+    }
+    static __device__ __forceinline__ F sel(bool p, F a, F b) { return {p ? a.d : b.d, p ? a.s : b.s}; }
+    static __device__ __forceinline__ int popd(F a) { return __popc(a.d); }
+};
 
-// a + b with the ternary-safety flag (signs simplified under s subset d)
-template <int RING, typename T> __device__ __forceinline__ Tv<T> add(Tv<T> a, Tv<T> b, bool &ok)
-{
-    const T d = a.d ^ b.d;
-    if (RING == FG_Z2) return {d, (T)0};
-    ok = ok && ((a.d & b.d & ~(a.s ^ b.s)) == 0);
-    return {d, (a.s | b.s) & d};
-}
-// a - b = a + (-b)
-template <int RING, typename T> __device__ __forceinline__ Tv<T> sub(Tv<T> a, Tv<T> b, bool &ok)
-{
-    if (RING == FG_Z2) return {a.d ^ b.d, (T)0};
-    return add<RING, T>(a, neg(b), ok);
-}
-template <int RING, typename T> __device__ __forceinline__ bool distinct(Tv<T> a, Tv<T> b)
-{
-    if (eq(a, b)) return false;
-    if (RING == FG_ZT && negeq(a, b)) return false;
-    return true;
-}
+// PZ2: digits only, arithmetic mod 2
+struct PZ2 {
+    typedef uint32_t F;
+    static constexpr int RING = FG_Z2;
+    static __device__ __forceinline__ F make(uint64_t d, uint64_t) { return (uint32_t)d; }
+    static __device__ __forceinline__ uint64_t dig(F a) { return a; }
+    static __device__ __forceinline__ uint64_t sgn(F) { return 0; }
+    static __device__ __forceinline__ bool zero(F a) { return a == 0; }
+    static __device__ __forceinline__ bool eq(F a, F b) { return a == b; }
+    static __device__ __forceinline__ bool negeq(F, F) { return false; }
+    static __device__ __forceinline__ F neg(F a) { return a; }
+    static __device__ __forceinline__ F abs(F a) { return a; }
+    static __device__ __forceinline__ bool first_neg(F) { return false; }
+    static __device__ __forceinline__ F add(F a, F b, bool &) { return a ^ b; }
+    static __device__ __forceinline__ F sub(F a, F b, bool &) { return a ^ b; }
+    static __device__ __forceinline__ F shfl(F a, int src) { return __shfl_sync(FULL, a, src); }
+    static __device__ __forceinline__ unsigned match(F a) { return __match_any_sync(FULL, a); }
+    static __device__ __forceinline__ F sel(bool p, F a, F b) { return p ? a : b; }
+    static __device__ __forceinline__ int popd(F a) { return __popc(a); }
+};
 
-template <typename T> struct Row { Tv<T> u, v, w; };
+template <class P> struct Row { typename P::F u, v, w; };
 
-template <typename T> __device__ __forceinline__ Tv<T> get(const Row<T> &r, int X)
+// role X in {0: U, 1: V, 2: W}, branch-free
+template <class P> __device__ __forceinline__ typename P::F get(const Row<P> &r, int X)
 {
-    Tv<T> o;
-    o.d = X == 0 ? r.u.d : (X == 1 ? r.v.d : r.w.d);
-    o.s = X == 0 ? r.u.s : (X == 1 ? r.v.s : r.w.s);
-    return o;
+    return P::sel(X & 2, r.w, P::sel(X & 1, r.v, r.u));
 }
-template <typename T> __device__ __forceinline__ void set(Row<T> &r, int X, Tv<T> x, bool pred)
+template <class P> __device__ __forceinline__ void set(Row<P> &r, int X, typename P::F x, bool pred)
 {
-    if (pred && X == 0) r.u = x;
-    if (pred && X == 1) r.v = x;
-    if (pred && X == 2) r.w = x;
+    r.u = P::sel(pred && X == 0, x, r.u);
+    r.v = P::sel(pred && X == 1, x, r.v);
+    r.w = P::sel(pred && X == 2, x, r.w);
 }
-template <typename T> __device__ __forceinline__ bool has_zero(const Row<T> &r)
+template <class P> __device__ __forceinline__ bool has_zero(const Row<P> &r)
 {
-    return r.u.d == 0 || r.v.d == 0 || r.w.d == 0;
+    return P::zero(r.u) || P::zero(r.v) || P::zero(r.w);
+}
+template <class P> __device__ __forceinline__ bool distinct(typename P::F a, typename P::F b)
+{
+    return !P::eq(a, b) && !P::negeq(a, b);
 }
 
 // PAPER:429 per row (R6): first nonzero of u, then v, made positive; w absorbs.
-// lowbit(d) = d & -d is the first nonzero position.
-template <int RING, typename T> __device__ __forceinline__ void normalize(Row<T> &r)
+template <class P> __device__ __forceinline__ void normalize(Row<P> &r)
 {
-    if (RING != FG_ZT) return;
-    const T nu = (r.u.s & (r.u.d & (T)(0 - r.u.d))) ? ~(T)0 : (T)0;
-    r.u.s ^= r.u.d & nu;
-    r.w.s ^= r.w.d & nu;
-    const T nv = (r.v.s & (r.v.d & (T)(0 - r.v.d))) ? ~(T)0 : (T)0;
-    r.v.s ^= r.v.d & nv;
-    r.w.s ^= r.w.d & nv;
+    if (P::RING != FG_ZT) return;
+    const bool nu = P::first_neg(r.u);
+    r.u = P::sel(nu, P::neg(r.u), r.u);
+    r.w = P::sel(nu, P::neg(r.w), r.w);
+    const bool nv = P::first_neg(r.v);
+    r.v = P::sel(nv, P::neg(r.v), r.v);
+    r.w = P::sel(nv, P::neg(r.w), r.w);
 }
 
-template <typename T, bool K16> __device__ __forceinline__ Tv<T> shfl(Tv<T> x, int src)
+template <class P> __device__ __forceinline__ Row<P> shfl_row(const Row<P> &r, int src)
 {
-    Tv<T> o;
-    if constexpr (sizeof(T) == 4 && K16) {
-        const uint32_t k = __shfl_sync(FULL, (uint32_t)(x.d | (x.s << 16)), src);
-        o.d = k & 0xffffu;
-        o.s = k >> 16;
-    } else {
-        o.d = __shfl_sync(FULL, x.d, src);
-        o.s = __shfl_sync(FULL, x.s, src);
-    }
+    Row<P> o;
+    o.u = P::shfl(r.u, src);
+    o.v = P::shfl(r.v, src);
+    o.w = P::shfl(r.w, src);
     return o;
-}
-template <int RING, typename T, bool K16> __device__ __forceinline__ Row<T> shfl_row(const Row<T> &r, int src)
-{
-    Row<T> o;
-    if (RING == FG_Z2) {
-        o.u.d = __shfl_sync(FULL, r.u.d, src); o.u.s = 0;
-        o.v.d = __shfl_sync(FULL, r.v.d, src); o.v.s = 0;
-        o.w.d = __shfl_sync(FULL, r.w.d, src); o.w.s = 0;
-    } else {
-        o.u = shfl<T, K16>(r.u, src);
-        o.v = shfl<T, K16>(r.v, src);
-        o.w = shfl<T, K16>(r.w, src);
-    }
-    return o;
-}
-
-// lanes holding the same factor value (all 32 lanes participate)
-template <int RING, typename T, bool K16> __device__ __forceinline__ unsigned match(Tv<T> x)
-{
-    if constexpr (sizeof(T) == 4) {
-        if (RING == FG_Z2) return __match_any_sync(FULL, (uint32_t)x.d);
-        if constexpr (K16) return __match_any_sync(FULL, (uint32_t)(x.d | (x.s << 16)));
-        else return __match_any_sync(FULL, (unsigned long long)x.d | ((unsigned long long)x.s << 32));
-    } else {
-        if (RING == FG_Z2) return __match_any_sync(FULL, (unsigned long long)x.d);
-        return __match_any_sync(FULL, (unsigned long long)x.d) &
-               __match_any_sync(FULL, (unsigned long long)x.s);
-    }
 }
 
 // R13 reducible(i, j) with row i = ri, row j = rj; merged = row i with C replaced
 // (x_C[i] + sigma x_C[j]), normalised.  Role pairs (A,B,C) in the order
 // (U,V,W), (U,W,V), (V,W,U) (PAPER:233-238 under any permutation).
-template <int RING, typename T> __device__ __forceinline__ bool reducible(const Row<T> &ri, const Row<T> &rj,
-                                                                          Row<T> &merged)
+template <class P> __device__ __forceinline__ bool reducible(const Row<P> &ri, const Row<P> &rj, Row<P> &merged)
 {
-    // (U,V,W): u and v shared, w merged (sigma = +1: B = V)
-    if (eq(ri.u, rj.u) && eq(ri.v, rj.v)) {
+    if (P::eq(ri.u, rj.u) && P::eq(ri.v, rj.v)) {
         bool ok = true;
-        Tv<T> c = add<RING, T>(ri.w, rj.w, ok);
-        if (ok) { merged = ri; merged.w = c; normalize<RING, T>(merged); return true; }
+        const typename P::F c = P::add(ri.w, rj.w, ok);
+        if (ok) { merged = ri; merged.w = c; normalize<P>(merged); return true; }
     }
-    // (U,W,V): u shared, w shared up to sign, v merged
-    if (eq(ri.u, rj.u)) {
-        int sg = eq(ri.w, rj.w) ? 1 : ((RING == FG_ZT && negeq(ri.w, rj.w)) ? -1 : 0);
-        if (sg) {
-            bool ok = true;
-            Tv<T> c = add<RING, T>(ri.v, sg > 0 ? rj.v : neg(rj.v), ok);
-            if (ok) { merged = ri; merged.v = c; normalize<RING, T>(merged); return true; }
-        }
+    const int sg = P::eq(ri.w, rj.w) ? 1 : (P::negeq(ri.w, rj.w) ? -1 : 0);
+    if (sg && P::eq(ri.u, rj.u)) {
+        bool ok = true;
+        const typename P::F c = P::add(ri.v, sg > 0 ? rj.v : P::neg(rj.v), ok);
+        if (ok) { merged = ri; merged.v = c; normalize<P>(merged); return true; }
     }
-    // (V,W,U): v shared, w shared up to sign, u merged
-    if (eq(ri.v, rj.v)) {
-        int sg = eq(ri.w, rj.w) ? 1 : ((RING == FG_ZT && negeq(ri.w, rj.w)) ? -1 : 0);
-        if (sg) {
-            bool ok = true;
-            Tv<T> c = add<RING, T>(ri.u, sg > 0 ? rj.u : neg(rj.u), ok);
-            if (ok) { merged = ri; merged.u = c; normalize<RING, T>(merged); return true; }
-        }
+    if (sg && P::eq(ri.v, rj.v)) {
+        bool ok = true;
+        const typename P::F c = P::add(ri.u, sg > 0 ? rj.u : P::neg(rj.u), ok);
+        if (ok) { merged = ri; merged.u = c; normalize<P>(merged); return true; }
     }
     return false;
 }

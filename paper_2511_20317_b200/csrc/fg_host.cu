@@ -31,6 +31,7 @@ struct DevMisc {         // small device-side scratch read back after every fg_w
     uint32_t verify_fail;
     uint32_t pad;
     unsigned long long restarted;
+    unsigned long long work_counter;
 };
 
 }  // namespace
@@ -434,6 +435,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.thr_expand = P.thr_expand; a.slack = P.expand_slack;
     a.q_planes = c->d_qplanes; a.q_meta = c->d_qmeta; a.q_count = &c->d_misc->q_count;
     a.q_cap = c->qcap; a.q_overflow = &c->d_misc->q_overflow; a.best_key = &c->d_misc->best_key;
+    a.work_counter = &c->d_misc->work_counter;
     VerifyArgs v;
     memset(&v, 0, sizeof(v));
     v.planes = c->d_qplanes; v.meta = c->d_qmeta; v.count_ptr = &c->d_misc->q_count; v.cap = c->qcap;
@@ -450,6 +452,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         a.steps = chunk;
         CK(cudaMemsetAsync(&c->d_misc->best_key, 0xff, sizeof(unsigned long long), c->stream));
         CK(cudaMemsetAsync(&c->d_misc->q_count, 0, sizeof(uint32_t), c->stream));
+        CK(cudaMemsetAsync(&c->d_misc->work_counter, 0, sizeof(unsigned long long), c->stream));
         CK(cudaEventRecord(c->ev0, c->stream));
         CK(fg_launch_walk(c->kind, a, c->num_sms, c->stream));
         CK(cudaEventRecord(c->ev1, c->stream));

@@ -56,6 +56,7 @@ struct WalkArgs {
     uint32_t *q_overflow;
     // local best key (R20): rank<<54 | additions<<36 | local walker index
     unsigned long long *best_key;
+    unsigned long long *work_counter;   // dynamic walker queue, zeroed before each launch
 };
 
 struct VerifyArgs {

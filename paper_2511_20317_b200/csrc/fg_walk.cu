@@ -48,10 +48,10 @@ __device__ __forceinline__ int nth_bit(uint32_t x, uint32_t t)
     return pos;
 }
 
-template <int RING, bool K16>
+template <class P>
 __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
 {
-    using T = uint32_t;
+    typedef typename P::F F;
     __shared__ uint32_t px_all[W32_WARPS][32 * PXS];
     __shared__ uint32_t rc_all[W32_WARPS][8];     // rare counters (lane 0 updates)
     uint32_t *px = px_all[threadIdx.x >> 5];
@@ -59,22 +59,26 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
     const int lane = threadIdx.x & 31;
     const unsigned lanebit = 1u << lane;
     const unsigned above = ~((lanebit << 1) - 1u);          // lanes > this one
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const int R = a.R;
     const uint64_t seed = a.seed;
     const uint32_t kf = a.k_flip;
 
-    for (int64_t wk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; wk < a.num_walkers;
-         wk += nwarps) {
+    // dynamic walker queue: warps that finish early take more walkers
+    auto grab = [&]() -> int64_t {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(a.work_counter, 1ull);
+        return (int64_t)__shfl_sync(FULL, v, 0);
+    };
+    for (int64_t wk = grab(); wk < a.num_walkers; wk = grab()) {
         // ---------------- load walker (coalesced: plane q of rows 0..31) ----------------
         const uint64_t *cp = a.cur + (size_t)wk * FG_PLANES * R;
         uint64_t *bw = a.best + (size_t)wk * FG_PLANES * R;
-        Row<T> row;
-        row.u.d = row.u.s = row.v.d = row.v.s = row.w.d = row.w.s = 0;
+        Row<P> row;
+        row.u = row.v = row.w = P::make(0, 0);
         if (lane < R) {
-            row.u.d = (T)cp[0 * R + lane]; row.u.s = (T)cp[1 * R + lane];
-            row.v.d = (T)cp[2 * R + lane]; row.v.s = (T)cp[3 * R + lane];
-            row.w.d = (T)cp[4 * R + lane]; row.w.s = (T)cp[5 * R + lane];
+            row.u = P::make(cp[0 * R + lane], cp[1 * R + lane]);
+            row.v = P::make(cp[2 * R + lane], cp[3 * R + lane]);
+            row.w = P::make(cp[4 * R + lane], cp[5 * R + lane]);
         }
         fg_whdr *hp = a.hdr + wk;
         int r = hp->r;
@@ -91,26 +95,24 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
 
         // masks of live lanes holding the same u / v / w-up-to-sign as this lane
         unsigned mU = 0, mV = 0, mWp = 0;
-        auto wabs = [&](Tv<T> w) {
-            const T nw = (w.s & (w.d & (T)(0 - w.d))) ? ~(T)0 : (T)0;
-            w.s ^= w.d & nw;
-            return w;
-        };
+        F wA = P::abs(row.w);                 // this lane's w up to sign (cached)
         auto compute_masks = [&]() {
             const unsigned act = r >= 32 ? FULL : ((1u << r) - 1u);
-            mU = match<RING, T, K16>(row.u) & act;
-            mV = match<RING, T, K16>(row.v) & act;
-            mWp = (RING == FG_ZT ? match<RING, T, K16>(wabs(row.w)) : match<RING, T, K16>(row.w)) & act;
+            wA = P::abs(row.w);
+            mU = P::match(row.u) & act;
+            mV = P::match(row.v) & act;
+            mWp = P::match(wA) & act;
         };
         // incremental update after rows ta != tb changed (all other rows unchanged)
         auto update_masks2 = [&](int ta, int tb) {
-            const Row<T> ra = shfl_row<RING, T, K16>(row, ta);
-            const Row<T> rb = shfl_row<RING, T, K16>(row, tb);
+            if (lane == ta || lane == tb) wA = P::abs(row.w);
+            const F ua_ = P::shfl(row.u, ta), ub_ = P::shfl(row.u, tb);
+            const F va_ = P::shfl(row.v, ta), vb_ = P::shfl(row.v, tb);
+            const F wa_k = P::shfl(wA, ta), wb_k = P::shfl(wA, tb);
             const bool live = lane < r;
-            const Tv<T> aw = wabs(row.w);
-            const bool ua = live && eq(row.u, ra.u), ub = live && eq(row.u, rb.u);
-            const bool va = live && eq(row.v, ra.v), vb = live && eq(row.v, rb.v);
-            const bool wa_ = live && eq(aw, wabs(ra.w)), wb_ = live && eq(aw, wabs(rb.w));
+            const bool ua = live && P::eq(row.u, ua_), ub = live && P::eq(row.u, ub_);
+            const bool va = live && P::eq(row.v, va_), vb = live && P::eq(row.v, vb_);
+            const bool wa_ = live && P::eq(wA, wa_k), wb_ = live && P::eq(wA, wb_k);
             const unsigned keep = ~((1u << ta) | (1u << tb));
             mU = (mU & keep) | ((unsigned)ua << ta) | ((unsigned)ub << tb);
             mV = (mV & keep) | ((unsigned)va << ta) | ((unsigned)vb << tb);
@@ -130,7 +132,7 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
             if (nwl >= 2 && wl1 != h) { if (n2 == 0) x0 = wl1; else x1 = wl1; n2++; }
             wl0 = x0; wl1 = x1; nwl = n2;
             if (h != last) {
-                const Row<T> mv = shfl_row<RING, T, K16>(row, last);
+                const Row<P> mv = shfl_row<P>(row, last);
                 if (lane == h) row = mv;
                 if (nwl >= 1 && wl0 == last) wl0 = h;
                 if (nwl >= 2 && wl1 == last) wl1 = h;
@@ -146,19 +148,19 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 wl0 = wl1;
                 nwl--;
                 if (t >= r) continue;
-                const Row<T> rt = shfl_row<RING, T, K16>(row, t);
+                const Row<P> rt = shfl_row<P>(row, t);
                 if (has_zero(rt)) {
                     remove_row(t, wl0, wl1, nwl);
                     bump(RC_ZERO, 1);
                     continue;
                 }
-                Row<T> merged = row;
-                const bool red = lane < r && lane != t && reducible<RING, T>(rt, row, merged);
+                Row<P> merged = row;
+                const bool red = lane < r && lane != t && reducible<P>(rt, row, merged);
                 const unsigned bal = __ballot_sync(FULL, red);
                 if (!bal) continue;
                 const int j = __ffs(bal) - 1;
                 const int lo = t < j ? t : j, hi = t < j ? j : t;
-                const Row<T> mg = shfl_row<RING, T, K16>(merged, j);
+                const Row<P> mg = shfl_row<P>(merged, j);
                 if (lane == lo) row = mg;
                 bump(RC_MERGE, 1);
                 remove_row(hi, wl0, wl1, nwl);
@@ -190,13 +192,13 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 while (cand) {
                     const int i = __ffs(cand) - 1;
                     cand &= cand - 1;
-                    const Row<T> ri = shfl_row<RING, T, K16>(row, i);
-                    Row<T> merged = row;
-                    const bool red = lane < r && lane > i && reducible<RING, T>(ri, row, merged);
+                    const Row<P> ri = shfl_row<P>(row, i);
+                    Row<P> merged = row;
+                    const bool red = lane < r && lane > i && reducible<P>(ri, row, merged);
                     const unsigned bal = __ballot_sync(FULL, red);
                     if (!bal) continue;
                     const int j = __ffs(bal) - 1;
-                    const Row<T> mg = shfl_row<RING, T, K16>(merged, j);
+                    const Row<P> mg = shfl_row<P>(merged, j);
                     if (lane == i) row = mg;
                     bump(RC_MERGE, 1);
                     int n0 = 0, x0 = 0, x1 = 0;
@@ -226,18 +228,18 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
             const int A = perm >> 1;
             const int B = (1161 >> (2 * perm)) & 3;
             const int Cr = 3 - A - B;
-            const Row<T> ri = shfl_row<RING, T, K16>(row, i);
-            const Row<T> rj = shfl_row<RING, T, K16>(row, j);
-            const Tv<T> ai = get(ri, A), aj = get(rj, A), bi = get(ri, B), bj = get(rj, B);
-            const Tv<T> ci = get(ri, Cr), cj = get(rj, Cr);
+            const Row<P> ri = shfl_row<P>(row, i);
+            const Row<P> rj = shfl_row<P>(row, j);
+            const F ai = get(ri, A), aj = get(rj, A), bi = get(ri, B), bj = get(rj, B);
+            const F ci = get(ri, Cr), cj = get(rj, Cr);
             bool ok = true;
             if (plus) {
-                if (!distinct<RING, T>(ai, aj) || !distinct<RING, T>(bi, bj) ||
-                    !distinct<RING, T>(ci, cj))
+                if (!distinct<P>(ai, aj) || !distinct<P>(bi, bj) ||
+                    !distinct<P>(ci, cj))
                     return false;
-                const Tv<T> t1 = add<RING, T>(bi, bj, ok);      // v_i + v_j
-                const Tv<T> t2 = sub<RING, T>(cj, ci, ok);      // w_j - w_i
-                const Tv<T> t3 = sub<RING, T>(aj, ai, ok);      // u_j - u_i
+                const F t1 = P::add(bi, bj, ok);      // v_i + v_j
+                const F t2 = P::sub(cj, ci, ok);      // w_j - w_i
+                const F t3 = P::sub(aj, ai, ok);      // u_j - u_i
                 if (!ok) return false;
                 set(row, B, t1, lane == i);
                 set(row, A, ai, lane == j);
@@ -246,15 +248,15 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 set(row, B, bj, lane == r);
                 set(row, Cr, cj, lane == r);
             } else {
-                if (!distinct<RING, T>(ai, aj)) return false;
-                const Tv<T> t3 = sub<RING, T>(ai, aj, ok);      // u_i - u_j
+                if (!distinct<P>(ai, aj)) return false;
+                const F t3 = P::sub(ai, aj, ok);      // u_i - u_j
                 if (!ok) return false;
                 set(row, A, aj, lane == i);
                 set(row, A, t3, lane == r);
                 set(row, B, bi, lane == r);
                 set(row, Cr, ci, lane == r);
             }
-            if (lane == i || lane == j || lane == r) normalize<RING, T>(row);
+            if (lane == i || lane == j || lane == r) normalize<P>(row);
             r++;
             compute_masks();
             return true;
@@ -269,15 +271,18 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 // lane L: Philox blocks 0 and 2 of step (step + L) -> px[L*9 + 0..7]
                 uint32_t o0, o1, o2, o3;
                 philox_block(seed, step + lane, wid, 0u, o0, o1, o2, o3);
-                px[lane * PXS + 0] = o0; px[lane * PXS + 1] = o1;
-                px[lane * PXS + 2] = o2; px[lane * PXS + 3] = o3;
+                // word 0 = draw 0; the three Bernoulli draws of the step pre-decided (R9)
+                px[lane * PXS + 0] = o0;
+                px[lane * PXS + 1] = (o1 < a.thr_eq ? 1u : 0u) | (o2 < a.thr_reduce ? 2u : 0u) |
+                                     (o3 < a.thr_expand ? 4u : 0u);
                 philox_block(seed, step + lane, wid, 2u, o0, o1, o2, o3);
                 px[lane * PXS + 4] = o0; px[lane * PXS + 5] = o1;
                 px[lane * PXS + 6] = o2; px[lane * PXS + 7] = o3;
                 __syncwarp();
                 boff = 0;
             }
-            const uint32_t *pw = px + boff * PXS;     // [attempt0, accept, reduce, expand_p, attempts 1..4]
+            const uint32_t *pw = px + boff * PXS;     // [draw 0, Bernoulli flags, -, -, draws 1..4]
+            const uint32_t bern = pw[1];
             uint32_t flags = 0;
             int alpha = 0, beta = 0, draws = 0;
             bool ok = false;
@@ -301,13 +306,14 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
 
             // ---- R11 try_flip: draw `att` evaluated by this lane with word x ----
             int e_al = 0, e_be = 0, e_Y = 0, e_Z = 0;
-            Tv<T> e_ny, e_nz;
+            F e_ny, e_nz;
             auto eval = [&](uint32_t x) -> bool {
                 const uint32_t k = __umulhi(x, 4u * nC);
                 const uint32_t idx = k >> 2;
                 const int d = k & 1, e = (k >> 1) & 1;
-                const int X = idx < nU ? 0 : (idx < nU + nV ? 1 : 2);
-                const uint32_t qq = idx - (X == 0 ? 0u : (X == 1 ? nU : nU + nV));
+                const uint32_t g1 = idx >= nU, g2 = idx >= nU + nV;
+                const int X = (int)(g1 + g2);
+                const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
                 const int sh = 10 * X;
                 int i = 0;
 #pragma unroll
@@ -319,20 +325,21 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 const unsigned mu_i = __shfl_sync(FULL, mU, i);
                 const unsigned mv_i = __shfl_sync(FULL, mV, i);
                 const unsigned mw_i = __shfl_sync(FULL, mWp, i);
-                const unsigned mm = (X == 0 ? mu_i : (X == 1 ? mv_i : mw_i)) & ~((2u << i) - 1u);
+                const unsigned mm = ((X & 2) ? mw_i : ((X & 1) ? mv_i : mu_i)) & ~((2u << i) - 1u);
                 const int j = nth_bit(mm, qq - ex_i);
                 const int al = d ? j : i, be = d ? i : j;
-                int Y, Z;
-                if (X == 0) { Y = 1; Z = 2; } else if (X == 1) { Y = 2; Z = 0; } else { Y = 0; Z = 1; }
-                if (e) { const int tt = Y; Y = Z; Z = tt; }
-                const Row<T> ra = shfl_row<RING, T, K16>(row, al);
-                const Row<T> rb = shfl_row<RING, T, K16>(row, be);
+                // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e:
+                // nibble 2X+e of 0x148269 holds Y | Z << 2
+                const unsigned yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
+                const int Y = yz & 3, Z = yz >> 2;
+                const Row<P> ra = shfl_row<P>(row, al);
+                const Row<P> rb = shfl_row<P>(row, be);
                 // sigma = -1 iff the shared factor is W and the two are negatives
-                const bool sneg = RING == FG_ZT && X == 2 && !eq(ra.w, rb.w);
+                const bool sneg = P::RING == FG_ZT && X == 2 && !P::eq(ra.w, rb.w);
                 bool v = true;
-                const Tv<T> yb = get(rb, Y);
-                e_ny = add<RING, T>(get(ra, Y), sneg ? neg(yb) : yb, v);     // y_a + s y_b
-                e_nz = sub<RING, T>(get(rb, Z), get(ra, Z), v);              // z_b - z_a
+                const F yb = get(rb, Y);
+                e_ny = P::add(get(ra, Y), P::sel(sneg, P::neg(yb), yb), v);     // y_a + s y_b
+                e_nz = P::sub(get(rb, Z), get(ra, Z), v);              // z_b - z_a
                 e_al = al; e_be = be; e_Y = Y; e_Z = Z;
                 return v;
             };
@@ -360,13 +367,13 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                     const int src = __ffs(win) - 1;
                     draws = base + src + 1;
                     const unsigned info = __shfl_sync(FULL, (unsigned)(e_al | (e_be << 8) | (e_Y << 16) | (e_Z << 18)), src);
-                    const Tv<T> ny = shfl<T, K16>(e_ny, src);
-                    const Tv<T> nz = shfl<T, K16>(e_nz, src);
+                    const F ny = P::shfl(e_ny, src);
+                    const F nz = P::shfl(e_nz, src);
                     alpha = info & 255;
                     beta = (info >> 8) & 255;
                     set(row, (info >> 16) & 3, ny, lane == alpha);
                     set(row, (info >> 18) & 3, nz, lane == beta);
-                    if (lane == alpha || lane == beta) normalize<RING, T>(row);
+                    if (lane == alpha || lane == beta) normalize<P>(row);
                     ok = true;
                 } else {
                     draws = kf;
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 }
                 // ---- PAPER:310-313 acceptance ----
                 bool acc = r < best;
-                if (!acc && r == best) acc = pw[1] < a.thr_eq;
+                if (!acc && r == best) acc = bern & 1u;
                 if (acc) {
                     const bool strict = r < best;
                     best = r;
@@ -403,12 +410,12 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                     flags |= 4u;
                     if (lane < R) {
                         const bool lv = lane < r;
-                        bw[0 * R + lane] = lv ? (uint64_t)row.u.d : 0;
-                        bw[1 * R + lane] = lv ? (uint64_t)row.u.s : 0;
-                        bw[2 * R + lane] = lv ? (uint64_t)row.v.d : 0;
-                        bw[3 * R + lane] = lv ? (uint64_t)row.v.s : 0;
-                        bw[4 * R + lane] = lv ? (uint64_t)row.w.d : 0;
-                        bw[5 * R + lane] = lv ? (uint64_t)row.w.s : 0;
+                        bw[0 * R + lane] = lv ? P::dig(row.u) : 0;
+                        bw[1 * R + lane] = lv ? P::sgn(row.u) : 0;
+                        bw[2 * R + lane] = lv ? P::dig(row.v) : 0;
+                        bw[3 * R + lane] = lv ? P::sgn(row.v) : 0;
+                        bw[4 * R + lane] = lv ? P::dig(row.w) : 0;
+                        bw[5 * R + lane] = lv ? P::sgn(row.w) : 0;
                     }
                     if (strict) {
                         flags |= 8u;
@@ -421,12 +428,12 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                             uint64_t *qp = a.q_planes + (size_t)slot * FG_PLANES * R;
                             if (lane < R) {
                                 const bool lv = lane < r;
-                                qp[0 * R + lane] = lv ? (uint64_t)row.u.d : 0;
-                                qp[1 * R + lane] = lv ? (uint64_t)row.u.s : 0;
-                                qp[2 * R + lane] = lv ? (uint64_t)row.v.d : 0;
-                                qp[3 * R + lane] = lv ? (uint64_t)row.v.s : 0;
-                                qp[4 * R + lane] = lv ? (uint64_t)row.w.d : 0;
-                                qp[5 * R + lane] = lv ? (uint64_t)row.w.s : 0;
+                                qp[0 * R + lane] = lv ? P::dig(row.u) : 0;
+                                qp[1 * R + lane] = lv ? P::sgn(row.u) : 0;
+                                qp[2 * R + lane] = lv ? P::dig(row.v) : 0;
+                                qp[3 * R + lane] = lv ? P::sgn(row.v) : 0;
+                                qp[4 * R + lane] = lv ? P::dig(row.w) : 0;
+                                qp[5 * R + lane] = lv ? P::sgn(row.w) : 0;
                             }
                             if (lane == 0) {
                                 fg_qmeta qm;
@@ -440,7 +447,7 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                     }
                 }
                 // ---- PAPER:315-317 reduce (R15) ----
-                if (pw[2] < a.thr_reduce) {
+                if (bern & 2u) {
                     c_red++;
                     flags |= 16u;
                     const unsigned two = ((mU & mV) | (mU & mWp) | (mV & mWp)) & ~lanebit;
@@ -450,7 +457,7 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                     }
                 }
                 // ---- PAPER:319-321 expand ----
-                if (pw[3] < a.thr_expand && r <= best + a.slack) {
+                if ((bern & 4u) && r <= best + a.slack) {
                     const bool ex = expand();
                     flags |= 32u | (ex ? 64u : 0u);
                     bump(RC_EOK, ex);
@@ -469,9 +476,9 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
         // ---------------- store walker ----------------
         uint64_t *cw = a.cur + (size_t)wk * FG_PLANES * R;
         if (lane < R) {
-            cw[0 * R + lane] = (uint64_t)row.u.d; cw[1 * R + lane] = (uint64_t)row.u.s;
-            cw[2 * R + lane] = (uint64_t)row.v.d; cw[3 * R + lane] = (uint64_t)row.v.s;
-            cw[4 * R + lane] = (uint64_t)row.w.d; cw[5 * R + lane] = (uint64_t)row.w.s;
+            cw[0 * R + lane] = P::dig(row.u); cw[1 * R + lane] = P::sgn(row.u);
+            cw[2 * R + lane] = P::dig(row.v); cw[3 * R + lane] = P::sgn(row.v);
+            cw[4 * R + lane] = P::dig(row.w); cw[5 * R + lane] = P::sgn(row.w);
         }
         // naive additions of the best -> local best key (R20); each lane
         // re-reads the best row it wrote itself
@@ -506,20 +513,19 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
     }
 }
 
-template <int RING, bool K16>
+template <class P>
 cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     int bps = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_w32<RING, K16>, W32_THREADS, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_w32<P>, W32_THREADS, 0);
     if (e != cudaSuccess) return e;
     if (bps < 1) bps = 1;
     const int64_t wpb = W32_WARPS;
-    const int64_t max_warps = (int64_t)num_sms * bps * wpb;
-    // even static partition: every warp runs exactly k walkers (or k-1)
-    const int64_t k = (a.num_walkers + max_warps - 1) / max_warps;
-    const int64_t nwarps = (a.num_walkers + k - 1) / k;
-    const int64_t blocks = (nwarps + wpb - 1) / wpb;
-    walk_w32<RING, K16><<<(unsigned)blocks, W32_THREADS, 0, st>>>(a);
+    // persistent: every resident warp pulls walkers from the queue
+    int64_t blocks = (int64_t)num_sms * bps;
+    const int64_t need = (a.num_walkers + wpb - 1) / wpb;
+    if (blocks > need) blocks = need;
+    walk_w32<P><<<(unsigned)blocks, W32_THREADS, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -537,9 +543,9 @@ int fg_pick_kernel(int ring, int maxlen, int R)
 const char *fg_kernel_kind_name(int kind)
 {
     switch (kind) {
-    case FG_K_W32_ZT_K16: return "walk_w32<ZT,key32>";
-    case FG_K_W32_ZT_K32: return "walk_w32<ZT,key64>";
-    case FG_K_W32_Z2_K32: return "walk_w32<Z2>";
+    case FG_K_W32_ZT_K16: return "walk_w32<P16>";
+    case FG_K_W32_ZT_K32: return "walk_w32<P32>";
+    case FG_K_W32_Z2_K32: return "walk_w32<PZ2>";
     default: return "none";
     }
 }
@@ -547,9 +553,9 @@ const char *fg_kernel_kind_name(int kind)
 cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     switch (kind) {
-    case FG_K_W32_ZT_K16: return launch_w32<FG_ZT, true>(a, num_sms, st);
-    case FG_K_W32_ZT_K32: return launch_w32<FG_ZT, false>(a, num_sms, st);
-    case FG_K_W32_Z2_K32: return launch_w32<FG_Z2, false>(a, num_sms, st);
+    case FG_K_W32_ZT_K16: return launch_w32<P16>(a, num_sms, st);
+    case FG_K_W32_ZT_K32: return launch_w32<P32>(a, num_sms, st);
+    case FG_K_W32_Z2_K32: return launch_w32<PZ2>(a, num_sms, st);
     default: return cudaErrorInvalidValue;
     }
 }
