@@ -139,6 +139,54 @@ struct PZ2 {
     static __device__ __forceinline__ int popd(F a) { return __popc(a); }
 };
 
+// P64: Z_T, <= 64 elements: (digits, signs) as two u64 words
+struct P64 {
+    struct F { uint64_t d, s; };
+    static constexpr int RING = FG_ZT;
+    static __device__ __forceinline__ F make(uint64_t d, uint64_t s) { return {d, s}; }
+    static __device__ __forceinline__ uint64_t dig(F a) { return a.d; }
+    static __device__ __forceinline__ uint64_t sgn(F a) { return a.s; }
+    static __device__ __forceinline__ bool zero(F a) { return a.d == 0; }
+    static __device__ __forceinline__ bool eq(F a, F b) { return a.d == b.d && a.s == b.s; }
+    static __device__ __forceinline__ bool negeq(F a, F b) { return a.d == b.d && a.s == (b.d ^ b.s) && a.d != 0; }
+    static __device__ __forceinline__ F neg(F a) { return {a.d, a.d ^ a.s}; }
+    static __device__ __forceinline__ F abs(F a) { return (a.s & (a.d & (0ull - a.d))) ? neg(a) : a; }
+    static __device__ __forceinline__ bool first_neg(F a) { return (a.s & (a.d & (0ull - a.d))) != 0; }
+    static __device__ __forceinline__ F add(F a, F b, bool &ok)
+    {
+        const uint64_t d = a.d ^ b.d;
+        ok = ok && ((a.d & b.d & ~(a.s ^ b.s)) == 0);
+        return {d, (a.s | b.s) & d};
+    }
+    static __device__ __forceinline__ F sub(F a, F b, bool &ok) { return add(a, neg(b), ok); }
+    static __device__ __forceinline__ F shfl(F a, int src)
+    {
+        return {__shfl_sync(FULL, a.d, src), __shfl_sync(FULL, a.s, src)};
+    }
+    static __device__ __forceinline__ F sel(bool p, F a, F b) { return {p ? a.d : b.d, p ? a.s : b.s}; }
+    static __device__ __forceinline__ int popd(F a) { return __popcll(a.d); }
+};
+
+// PZ64: Z_2, <= 64 elements
+struct PZ64 {
+    typedef uint64_t F;
+    static constexpr int RING = FG_Z2;
+    static __device__ __forceinline__ F make(uint64_t d, uint64_t) { return d; }
+    static __device__ __forceinline__ uint64_t dig(F a) { return a; }
+    static __device__ __forceinline__ uint64_t sgn(F) { return 0; }
+    static __device__ __forceinline__ bool zero(F a) { return a == 0; }
+    static __device__ __forceinline__ bool eq(F a, F b) { return a == b; }
+    static __device__ __forceinline__ bool negeq(F, F) { return false; }
+    static __device__ __forceinline__ F neg(F a) { return a; }
+    static __device__ __forceinline__ F abs(F a) { return a; }
+    static __device__ __forceinline__ bool first_neg(F) { return false; }
+    static __device__ __forceinline__ F add(F a, F b, bool &) { return a ^ b; }
+    static __device__ __forceinline__ F sub(F a, F b, bool &) { return a ^ b; }
+    static __device__ __forceinline__ F shfl(F a, int src) { return __shfl_sync(FULL, a, src); }
+    static __device__ __forceinline__ F sel(bool p, F a, F b) { return p ? a : b; }
+    static __device__ __forceinline__ int popd(F a) { return __popcll(a); }
+};
+
 template <class P> struct Row { typename P::F u, v, w; };
 
 // role X in {0: U, 1: V, 2: W}, branch-free

@@ -71,7 +71,11 @@ struct VerifyArgs {
 };
 
 // launchers (fg_walk.cu / fg_verify.cu); return cudaError_t
-enum fg_kernel_kind { FG_K_NONE = 0, FG_K_W32_ZT_K16, FG_K_W32_ZT_K32, FG_K_W32_Z2_K32 };
+enum fg_kernel_kind { FG_K_NONE = 0, FG_K_W32_ZT_K16, FG_K_W32_ZT_K32, FG_K_W32_Z2_K32,
+                      FG_K_WM_P16, FG_K_WM_P32, FG_K_WM_P64, FG_K_WM_Z2, FG_K_WM_Z64 };
+int fg_multi_ns(int R);
+int fg_multi_kind(int ring, int maxlen, int R);
+cudaError_t fg_launch_walk_multi(int kind, int ns, const WalkArgs &a, int num_sms, cudaStream_t st);
 int fg_pick_kernel(int ring, int maxlen, int R);
 const char *fg_kernel_kind_name(int kind);
 cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);

@@ -531,13 +531,17 @@ cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
 
 }  // namespace
 
-// R <= 32 implies every factor has <= 32 elements (the matmul tensor's rank is at
-// least max(mn, np, pm)), so the warp kernel only needs 32-bit factor words.
+// R <= 32: the warp kernel (every factor then has <= 32 elements: the matmul
+// tensor's rank is at least max(mn, np, pm)).  33 <= R <= 512: the multi-row kernel
+// (fg_walk_multi.cu) with the narrowest factor layout that fits.
 int fg_pick_kernel(int ring, int maxlen, int R)
 {
-    if (R > 32 || maxlen > 32) return FG_K_NONE;
-    if (ring == FG_ZT) return maxlen <= 16 ? FG_K_W32_ZT_K16 : FG_K_W32_ZT_K32;
-    return FG_K_W32_Z2_K32;
+    if (R <= 32) {
+        if (maxlen > 32) return FG_K_NONE;
+        if (ring == FG_ZT) return maxlen <= 16 ? FG_K_W32_ZT_K16 : FG_K_W32_ZT_K32;
+        return FG_K_W32_Z2_K32;
+    }
+    return fg_multi_kind(ring, maxlen, R);
 }
 
 const char *fg_kernel_kind_name(int kind)
@@ -546,6 +550,11 @@ const char *fg_kernel_kind_name(int kind)
     case FG_K_W32_ZT_K16: return "walk_w32<P16>";
     case FG_K_W32_ZT_K32: return "walk_w32<P32>";
     case FG_K_W32_Z2_K32: return "walk_w32<PZ2>";
+    case FG_K_WM_P16: return "walk_wm<P16>";
+    case FG_K_WM_P32: return "walk_wm<P32>";
+    case FG_K_WM_P64: return "walk_wm<P64>";
+    case FG_K_WM_Z2: return "walk_wm<PZ2>";
+    case FG_K_WM_Z64: return "walk_wm<PZ64>";
     default: return "none";
     }
 }
@@ -556,6 +565,6 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_W32_ZT_K16: return launch_w32<P16>(a, num_sms, st);
     case FG_K_W32_ZT_K32: return launch_w32<P32>(a, num_sms, st);
     case FG_K_W32_Z2_K32: return launch_w32<PZ2>(a, num_sms, st);
-    default: return cudaErrorInvalidValue;
+    default: return fg_launch_walk_multi(kind, fg_multi_ns(a.R), a, num_sms, st);
     }
 }

@@ -213,3 +213,51 @@ def test_restart_matches_oracle(fg, orc):
         w.walk(300, 3)
         assert w.digest == got["digest"][k] and w.r == got["r"][k]
         assert np.array_equal(w.rows(), got["rows"][k][: w.r])
+
+
+# ---------------- the multi-row kernel (33 <= R <= 512): configs C3-C5 ----------------
+MULTI_CASES = [
+    # (format, ring, R, walkers, sampled, steps)
+    ((4, 4, 4), ZT, 96, 512, 24, 2500),      # C3 Z_T, layout P16, NS 3
+    ((4, 4, 4), Z2, 96, 512, 24, 2500),      # C3 Z_2, layout PZ2
+    ((5, 5, 5), ZT, 160, 256, 12, 1200),     # C4, layout P32, NS 5
+    ((3, 3, 3), ZT, 33, 300, 24, 3000),      # ragged R (NS 2), ranks cross 32
+    ((3, 3, 3), Z2, 64, 300, 24, 3000),
+    ((4, 4, 4), ZT, 64, 200, 16, 2000),      # R = naive rank: every expand rejected
+    ((4, 5, 12), ZT, 256, 64, 6, 400),       # C5 formats, layout P64
+    ((6, 7, 9), ZT, 416, 48, 4, 250),
+    ((4, 5, 12), Z2, 256, 64, 6, 400),       # layout PZ64
+]
+
+
+@pytest.mark.parametrize("case", MULTI_CASES, ids=lambda c: f"{c[0]}-{'ZT' if c[1] == 0 else 'Z2'}-R{c[2]}")
+def test_multi_row_kernel_parity(fg, orc, case):
+    (m, n, p), ring, R, W, k, steps = case
+    g = _ctx(fg, m, n, p, ring, R, W, base=77)
+    assert g.kernel_name.startswith("walk_wm")
+    g.seed_naive()
+    seed = 0x2511203170000000 + 2 + ring
+    half = steps // 2
+    g.walk(half, seed)
+    g.walk(steps - half, seed)                 # phase split inside the comparison
+    got = g.get_walkers()
+    ids = sample_walkers(W, k, seed=R + ring)
+    ref = orc.run_walkers(m, n, p, ring, R, 0, 0, steps, seed, ids=ids + 77)
+    _assert_same(got, ref, idx=ids, what=f"multi {(m, n, p)} ring {ring} R {R}")
+    st = g.stats()
+    assert st["verify_fail"] == 0 and st["queue_overflow"] == 0
+    cur = [got["rows"][w][: got["r"][w]] for w in range(0, W, max(1, W // 16))]
+    ok, _ = g.verify_batch(cur)
+    assert np.all(ok == 1)
+
+
+def test_multi_row_seeded_pool_and_restart(fg, orc):
+    """Strassen seed (rank 7, no flip candidates) in the multi-row kernel (R = 40),
+    then an import + restart: trajectories still match the oracle."""
+    _, _, _, strassen = load_scheme("sec36_after.txt")
+    g = _ctx(fg, 2, 2, 2, ZT, 40, 20, base=3)
+    g.seed_pool(strassen)
+    g.walk(800, 11)
+    got = g.get_walkers()
+    ref = orc.run_walkers(2, 2, 2, ZT, 40, 20, 3, 800, 11, seed_coeffs=strassen)
+    _assert_same(got, ref, what="multi seed_pool")
