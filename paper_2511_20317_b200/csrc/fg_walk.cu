@@ -31,21 +31,16 @@ using namespace fgd;
 
 namespace {
 
-// position of the t-th (0-based) set bit of x; x has more than t set bits
+// position of the t-th (0-based) set bit of x; x has more than t set bits.  t is
+// almost always 0..2 (flip classes are small), so three predicated clears and a
+// find-first cover it; larger t takes a short loop.
 __device__ __forceinline__ int nth_bit(uint32_t x, uint32_t t)
 {
-    int pos = 0;
-    uint32_t c = __popc(x & 0xffffu);
-    if (t >= c) { t -= c; x >>= 16; pos += 16; }
-    c = __popc(x & 0xffu);
-    if (t >= c) { t -= c; x >>= 8; pos += 8; }
-    c = __popc(x & 0xfu);
-    if (t >= c) { t -= c; x >>= 4; pos += 4; }
-    c = __popc(x & 0x3u);
-    if (t >= c) { t -= c; x >>= 2; pos += 2; }
-    c = x & 1u;
-    if (t >= c) pos += 1;
-    return pos;
+    x = t > 0 ? (x & (x - 1u)) : x;
+    x = t > 1 ? (x & (x - 1u)) : x;
+    x = t > 2 ? (x & (x - 1u)) : x;
+    for (uint32_t k = 3; k < t; ++k) x &= x - 1u;
+    return __ffs(x) - 1;
 }
 
 template <class P>
@@ -315,11 +310,12 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 const int X = (int)(g1 + g2);
                 const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
                 const int sh = 10 * X;
+                const unsigned fm = 1023u << sh, qs = qq << sh;   // compare fields in place
                 int i = 0;
 #pragma unroll
                 for (int st = 16; st >= 1; st >>= 1) {
-                    const unsigned v = (__shfl_sync(FULL, incl, i + st - 1) >> sh) & 1023u;
-                    i += (v <= qq) ? st : 0;
+                    const unsigned v = __shfl_sync(FULL, incl, i | (st - 1)) & fm;
+                    i |= (v <= qs) ? st : 0;
                 }
                 const unsigned ex_i = (__shfl_sync(FULL, excl, i) >> sh) & 1023u;
                 const unsigned mu_i = __shfl_sync(FULL, mU, i);
