@@ -81,6 +81,7 @@ struct P16 {
     }
     static __device__ __forceinline__ F sub(F a, F b, bool &ok) { return add(a, neg(b), ok); }
     static __device__ __forceinline__ F shfl(F a, int src) { return __shfl_sync(FULL, a, src); }
+    static __device__ __forceinline__ F shflm(unsigned m, F a, int src) { return __shfl_sync(m, a, src); }
     static __device__ __forceinline__ unsigned match(F a) { return __match_any_sync(FULL, a); }
     static __device__ __forceinline__ F sel(bool p, F a, F b) { return p ? a : b; }
     static __device__ __forceinline__ int popd(F a) { return __popc(a & 0xffffu); }
@@ -110,6 +111,10 @@ struct P32 {
     {
         return {__shfl_sync(FULL, a.d, src), __shfl_sync(FULL, a.s, src)};
     }
+    static __device__ __forceinline__ F shflm(unsigned m, F a, int src)
+    {
+        return {__shfl_sync(m, a.d, src), __shfl_sync(m, a.s, src)};
+    }
     static __device__ __forceinline__ unsigned match(F a)
     {
         return __match_any_sync(FULL, (unsigned long long)a.d | ((unsigned long long)a.s << 32));
@@ -134,6 +139,7 @@ struct PZ2 {
     static __device__ __forceinline__ F add(F a, F b, bool &) { return a ^ b; }
     static __device__ __forceinline__ F sub(F a, F b, bool &) { return a ^ b; }
     static __device__ __forceinline__ F shfl(F a, int src) { return __shfl_sync(FULL, a, src); }
+    static __device__ __forceinline__ F shflm(unsigned m, F a, int src) { return __shfl_sync(m, a, src); }
     static __device__ __forceinline__ unsigned match(F a) { return __match_any_sync(FULL, a); }
     static __device__ __forceinline__ F sel(bool p, F a, F b) { return p ? a : b; }
     static __device__ __forceinline__ int popd(F a) { return __popc(a); }

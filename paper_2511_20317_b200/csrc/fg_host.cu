@@ -32,6 +32,7 @@ struct DevMisc {         // small device-side scratch read back after every fg_w
     uint32_t pad;
     unsigned long long restarted;
     unsigned long long work_counter;
+    uint32_t dbgbuf[16];
 };
 
 }  // namespace
@@ -436,6 +437,8 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.q_planes = c->d_qplanes; a.q_meta = c->d_qmeta; a.q_count = &c->d_misc->q_count;
     a.q_cap = c->qcap; a.q_overflow = &c->d_misc->q_overflow; a.best_key = &c->d_misc->best_key;
     a.work_counter = &c->d_misc->work_counter;
+    a.dbg = getenv("FG_DBG") ? (uint32_t)strtoul(getenv("FG_DBG"), nullptr, 0) : 0u;
+    a.dbgbuf = c->d_misc->dbgbuf;
     VerifyArgs v;
     memset(&v, 0, sizeof(v));
     v.planes = c->d_qplanes; v.meta = c->d_qmeta; v.count_ptr = &c->d_misc->q_count; v.cap = c->qcap;
@@ -470,6 +473,9 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         verified += std::min(hm.q_count, c->qcap);
         remaining -= chunk;
     } while (remaining > 0);
+    if (a.dbg && hm.dbgbuf[0])
+        fprintf(stderr, "libfg dbg: %u %u %u %u %u %u %u %u %u %u\n", hm.dbgbuf[0], hm.dbgbuf[1], hm.dbgbuf[2],
+                hm.dbgbuf[3], hm.dbgbuf[4], hm.dbgbuf[5], hm.dbgbuf[6], hm.dbgbuf[7], hm.dbgbuf[8], hm.dbgbuf[9]);
     int rc = refresh_local_best(c, hm.best_key);
     if (rc != FG_OK) return rc;
     c->st_vfail += hm.verify_fail;

@@ -57,6 +57,8 @@ struct WalkArgs {
     // local best key (R20): rank<<54 | additions<<36 | local walker index
     unsigned long long *best_key;
     unsigned long long *work_counter;   // dynamic walker queue, zeroed before each launch
+    uint32_t dbg;                       // debug switches (env FG_DBG), 0 in production
+    uint32_t *dbgbuf;                   // 16 words of debug output (first error wins)
 };
 
 struct VerifyArgs {
@@ -72,7 +74,9 @@ struct VerifyArgs {
 
 // launchers (fg_walk.cu / fg_verify.cu); return cudaError_t
 enum fg_kernel_kind { FG_K_NONE = 0, FG_K_W32_ZT_K16, FG_K_W32_ZT_K32, FG_K_W32_Z2_K32,
-                      FG_K_WM_P16, FG_K_WM_P32, FG_K_WM_P64, FG_K_WM_Z2, FG_K_WM_Z64 };
+                      FG_K_WM_P16, FG_K_WM_P32, FG_K_WM_P64, FG_K_WM_Z2, FG_K_WM_Z64,
+                      FG_K_H16_P16, FG_K_H16_P32, FG_K_H16_Z2 };
+cudaError_t fg_launch_walk_h16(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 int fg_multi_ns(int R);
 int fg_multi_kind(int ring, int maxlen, int R);
 cudaError_t fg_launch_walk_multi(int kind, int ns, const WalkArgs &a, int num_sms, cudaStream_t st);

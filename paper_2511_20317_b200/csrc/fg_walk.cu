@@ -21,6 +21,8 @@
 //     exact skip through the masks), expand (R16).
 // Independent of oracle/; parity is checked by tests/test_gpu_parity.py.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include "fg_device.cuh"
 
 using namespace fgd;
@@ -530,12 +532,19 @@ cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
 // R <= 32: the warp kernel (every factor then has <= 32 elements: the matmul
 // tensor's rank is at least max(mn, np, pm)).  33 <= R <= 512: the multi-row kernel
 // (fg_walk_multi.cu) with the narrowest factor layout that fits.
+// For R <= 32 the default is two walkers per warp (fg_walk_h16.cu); the environment
+// variable FG_WALK_KERNEL=w32 selects the one-walker-per-warp kernel (A/B tests).
 int fg_pick_kernel(int ring, int maxlen, int R)
 {
     if (R <= 32) {
         if (maxlen > 32) return FG_K_NONE;
-        if (ring == FG_ZT) return maxlen <= 16 ? FG_K_W32_ZT_K16 : FG_K_W32_ZT_K32;
-        return FG_K_W32_Z2_K32;
+        const char *env = getenv("FG_WALK_KERNEL");
+        const bool w32 = env && strcmp(env, "w32") == 0;
+        if (ring == FG_ZT) {
+            if (w32) return maxlen <= 16 ? FG_K_W32_ZT_K16 : FG_K_W32_ZT_K32;
+            return maxlen <= 16 ? FG_K_H16_P16 : FG_K_H16_P32;
+        }
+        return w32 ? FG_K_W32_Z2_K32 : FG_K_H16_Z2;
     }
     return fg_multi_kind(ring, maxlen, R);
 }
@@ -551,6 +560,9 @@ const char *fg_kernel_kind_name(int kind)
     case FG_K_WM_P64: return "walk_wm<P64>";
     case FG_K_WM_Z2: return "walk_wm<PZ2>";
     case FG_K_WM_Z64: return "walk_wm<PZ64>";
+    case FG_K_H16_P16: return "walk_h16<P16>";
+    case FG_K_H16_P32: return "walk_h16<P32>";
+    case FG_K_H16_Z2: return "walk_h16<PZ2>";
     default: return "none";
     }
 }
@@ -561,6 +573,9 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_W32_ZT_K16: return launch_w32<P16>(a, num_sms, st);
     case FG_K_W32_ZT_K32: return launch_w32<P32>(a, num_sms, st);
     case FG_K_W32_Z2_K32: return launch_w32<PZ2>(a, num_sms, st);
+    case FG_K_H16_P16:
+    case FG_K_H16_P32:
+    case FG_K_H16_Z2: return fg_launch_walk_h16(kind, a, num_sms, st);
     default: return fg_launch_walk_multi(kind, fg_multi_ns(a.R), a, num_sms, st);
     }
 }
