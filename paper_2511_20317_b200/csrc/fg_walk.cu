@@ -532,14 +532,15 @@ cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
 // R <= 32: the warp kernel (every factor then has <= 32 elements: the matmul
 // tensor's rank is at least max(mn, np, pm)).  33 <= R <= 512: the multi-row kernel
 // (fg_walk_multi.cu) with the narrowest factor layout that fits.
-// For R <= 32 the default is two walkers per warp (fg_walk_h16.cu); the environment
-// variable FG_WALK_KERNEL=w32 selects the one-walker-per-warp kernel (A/B tests).
+// For R <= 32 the default is one walker per warp (this file); FG_WALK_KERNEL=h16
+// selects the two-walkers-per-warp kernel (fg_walk_h16.cu; parity-exact, measured
+// 1.82 vs 1.92 G flip-steps/s on C2, profiles/r01_ncu_walk_h16.txt).
 int fg_pick_kernel(int ring, int maxlen, int R)
 {
     if (R <= 32) {
         if (maxlen > 32) return FG_K_NONE;
         const char *env = getenv("FG_WALK_KERNEL");
-        const bool w32 = env && strcmp(env, "w32") == 0;
+        const bool w32 = !(env && strcmp(env, "h16") == 0);
         if (ring == FG_ZT) {
             if (w32) return maxlen <= 16 ? FG_K_W32_ZT_K16 : FG_K_W32_ZT_K32;
             return maxlen <= 16 ? FG_K_H16_P16 : FG_K_H16_P32;

@@ -21,6 +21,9 @@ using namespace fgd;
 #define H16_THREADS 128
 #define H16_WARPS (H16_THREADS / 32)
 #define PXS 9
+#ifndef H16_MINB
+#define H16_MINB 6
+#endif
 
 namespace {
 
@@ -39,7 +42,7 @@ template <class P> struct Ev {
 };
 
 template <class P>
-__global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
+__global__ void __launch_bounds__(H16_THREADS, H16_MINB) walk_h16(WalkArgs a)
 {
     typedef typename P::F F;
     __shared__ F sR_all[H16_WARPS][2][3][32];          // row keys   [half][role][row]
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
         // code is the one-walker-per-warp routine of fg_walk.cu.  which: 0 = R12 local
         // reduction of rows (ta, tb), 1 = R15 reduce_all, 2 = R16 expand.  Returns the
         // walker's new rank.
-        auto rare = [&](int hs, int which, int ta, int tb) -> int {
+        auto rare = [&](int hs, int which, int ta, int tb, int &ei, int &ej) -> int {
             F(*S)[32] = sR_all[wib][hs];
             uint32_t *RC = rc_all[wib][hs];
             int rr = __shfl_sync(FULL, r, hs << 4);
@@ -278,6 +281,8 @@ __global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
                     if (done) {
                         if (lane == i || lane == j || lane == rr) normalize<P>(row);
                         rr++;
+                        ei = i;
+                        ej = j;
                     }
                 }
                 bumpr(done ? RC_EOK : RC_EREJ, 1);
@@ -286,6 +291,27 @@ __global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
             S[0][lane] = row.u; S[1][lane] = row.v; S[2][lane] = row.w;
             __syncwarp();
             return rr;
+        };
+        // incremental class masks after row t of half hs changed (all lanes call;
+        // lanes of half hs apply): bit t of every live row's masks, full masks of t
+        auto upd_row = [&](int hs, int t) {
+            const bool mine = h == hs;
+            const bool l0 = k < r, l1 = 16 + k < r;
+            const F tu = sR[0][t], tv = sR[1][t], ta = P::abs(sR[2][t]);
+            const bool u0 = l0 && P::eq(row0.u, tu), v0 = l0 && P::eq(row0.v, tv), w0 = l0 && P::eq(wA0, ta);
+            const bool u1 = l1 && P::eq(row1.u, tu), v1 = l1 && P::eq(row1.v, tv), w1 = l1 && P::eq(wA1, ta);
+            const unsigned MU = __byte_perm(__ballot_sync(FULL, u0), __ballot_sync(FULL, u1), prm);
+            const unsigned MV = __byte_perm(__ballot_sync(FULL, v0), __ballot_sync(FULL, v1), prm);
+            const unsigned MW = __byte_perm(__ballot_sync(FULL, w0), __ballot_sync(FULL, w1), prm);
+            if (mine) {
+                const unsigned bt = 1u << t;
+                mU0 = (mU0 & ~bt) | (u0 ? bt : 0u); mV0 = (mV0 & ~bt) | (v0 ? bt : 0u); mW0 = (mW0 & ~bt) | (w0 ? bt : 0u);
+                mU1 = (mU1 & ~bt) | (u1 ? bt : 0u); mV1 = (mV1 & ~bt) | (v1 ? bt : 0u); mW1 = (mW1 & ~bt) | (w1 ? bt : 0u);
+                if (k == (t & 15)) {
+                    if (t >> 4) { mU1 = MU; mV1 = MV; mW1 = MW; }
+                    else { mU0 = MU; mV0 = MV; mW0 = MW; }
+                }
+            }
         };
         // this half reloads its rows from its mirror and rebuilds its masks
         auto reload = [&]() {
@@ -488,7 +514,8 @@ __global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
                     for (int hs = 0; hs < 2; ++hs) {
                         if (!(nl & (1u << (hs << 4)))) continue;
                         const int ta = __shfl_sync(FULL, alpha, hs << 4), tb = __shfl_sync(FULL, beta, hs << 4);
-                        const int nr = rare(hs, 0, ta, tb);
+                        int e0, e1;
+                        const int nr = rare(hs, 0, ta, tb, e0, e1);
                         if (h == hs) { r = nr; reload(); }
                         __syncwarp();
                     }
@@ -533,7 +560,7 @@ __global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
                 flags |= red ? 16u : 0u;
                 const unsigned two0 = ((mU0 & mV0) | (mU0 & mW0) | (mV0 & mW0)) & ~(1u << k);
                 const unsigned two1 = ((mU1 & mV1) | (mU1 & mW1) | (mV1 & mW1)) & ~(1u << (16 + k));
-                const bool cnd = (k < r && (has_zero(row0) || two0 != 0)) || (16 + k < r && (has_zero(row1) || two1 != 0));
+                const bool cnd = (two0 | two1) != 0;   // dead rows have empty masks; R12 left no zero factor
                 const unsigned bR = __ballot_sync(FULL, cnd);        // every lane votes (no short circuit)
                 const bool needR = red && (bR & hm) != 0;
                 const unsigned nrm = (a.dbg & 2u) ? 0u : __ballot_sync(FULL, needR);
@@ -541,7 +568,8 @@ __global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
 #pragma unroll 1
                     for (int hs = 0; hs < 2; ++hs) {
                         if (!(nrm & (1u << (hs << 4)))) continue;
-                        const int nr = rare(hs, 1, 0, 0);
+                        int e0, e1;
+                        const int nr = rare(hs, 1, 0, 0, e0, e1);
                         if (h == hs) { r = nr; reload(); }
                         __syncwarp();
                     }
@@ -556,11 +584,26 @@ __global__ void __launch_bounds__(H16_THREADS, 8) walk_h16(WalkArgs a)
 #pragma unroll 1
                     for (int hs = 0; hs < 2; ++hs) {
                         if (!(nx & (1u << (hs << 4)))) continue;
-                        const int nr = rare(hs, 2, 0, 0);
+                        int ei = 0, ej = 0;
+                        const int rold = __shfl_sync(FULL, r, hs << 4);
+                        const int nr = rare(hs, 2, 0, 0, ei, ej);
+                        const bool ex = nr != rold;
                         if (h == hs) {
-                            const bool ex = nr != r;
                             flags |= (fb ? 2u : 32u) | (ex ? 64u : 0u);
-                            if (ex) { r = nr; reload(); }
+                            if (ex) {
+                                r = nr;
+                                row0.u = sR[0][k]; row0.v = sR[1][k]; row0.w = sR[2][k];
+                                row1.u = sR[0][16 + k]; row1.v = sR[1][16 + k]; row1.w = sR[2][16 + k];
+                                wA0 = P::abs(row0.w);
+                                wA1 = P::abs(row1.w);
+                            }
+                        }
+                        if (ex) {
+                            // incremental masks for the two changed rows and the new row
+                            upd_row(hs, ei);
+                            upd_row(hs, ej);
+                            upd_row(hs, rold);
+                            if (h == hs) store_masks();
                         }
                         __syncwarp();
                     }
