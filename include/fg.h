@@ -67,8 +67,16 @@ typedef struct fg_params {
     uint32_t thr_expand;    /* p_expand: default 0.01 -> 42949672 */
     int32_t  expand_slack;  /* Alg. 1 "best_rank + 2": default 2 */
     uint32_t phase_steps;   /* steps per kernel launch inside fg_walk (0 = all in one) */
-    uint32_t flags;         /* reserved, must be 0 */
+    uint32_t flags;         /* 0, or FG_FLAG_COMPLEXITY */
 } fg_params;
+
+/* fg_params.flags: naive-additive-complexity minimisation ("random flips
+   without reduction edges", Table 4; reading R24 in DESIGN.md): each
+   step is try_flip only -- a draw producing a zero factor is rejected, no local or
+   global reduction, no expand, so the rank never changes -- and the best scheme is
+   the minimum of (rank, naive additions PAPER:656), ties replaced with the 1%
+   plateau acceptance.  Every strict improvement is verified. */
+#define FG_FLAG_COMPLEXITY 1u
 
 typedef struct fg_ctx fg_ctx;   /* opaque: owns the device pool and its host mirror */
 
@@ -127,13 +135,14 @@ int fg_best(const fg_ctx *ctx, int *rank, int *naive_additions, int64_t *walker_
             int8_t *coeffs_out);
 
 /* Bulk read of local walkers [w_begin, w_end) for parity and debugging.  Any
-   output may be NULL.  Per walker: r, best_r, digest,
+   output may be NULL.  Per walker: r, best_r, naive additions of the best scheme,
+   digest,
    step index, FG_NCNT counters (steps, draws, flips, flip_fail, expand_ok,
    expand_reject, merges, zero_removed, best_copies, improvements, reduce_calls,
    verify_fail), and r_cap rows (zero-padded) of the current and best schemes. */
 int fg_get_walkers(const fg_ctx *ctx, int64_t w_begin, int64_t w_end, int32_t *r,
-                   int32_t *best_r, uint64_t *digest, uint64_t *step, uint64_t *cnt,
-                   int8_t *rows, int8_t *best);
+                   int32_t *best_r, int32_t *best_adds, uint64_t *digest, uint64_t *step,
+                   uint64_t *cnt, int8_t *rows, int8_t *best);
 
 /* Single-walker convenience form of fg_get_walkers. */
 int fg_get_walker(const fg_ctx *ctx, int64_t w, int *rank, int *best_rank, uint64_t *digest,

@@ -52,6 +52,7 @@ typedef struct {
     uint32_t thr_reduce;    /* p_reduce threshold */
     uint32_t thr_expand;    /* p_expand threshold */
     int32_t  expand_slack;  /* "best_rank + 2" */
+    uint32_t mode;          /* 0 = Alg. 1 walk, 1 = naive-complexity minimisation (R24) */
 } or_params;
 
 typedef struct {
@@ -59,6 +60,7 @@ typedef struct {
     int len[3];             /* m*n, n*p, p*m */
     int r;                  /* current rank */
     int best_r;
+    int best_adds;          /* naive additions of the best scheme */
     uint64_t walker_id;     /* global id, Philox counter word 2 (R8) */
     uint64_t step;          /* Alg.1 iteration index since seeding (R8) */
     uint64_t digest;        /* running event digest */

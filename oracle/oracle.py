@@ -35,12 +35,12 @@ def build_oracle(force: bool = False) -> str:
 class OracleParams(C.Structure):
     _fields_ = [("k_flip", C.c_uint32), ("thr_accept_eq", C.c_uint32),
                 ("thr_reduce", C.c_uint32), ("thr_expand", C.c_uint32),
-                ("expand_slack", C.c_int32)]
+                ("expand_slack", C.c_int32), ("mode", C.c_uint32)]
 
     @classmethod
     def default(cls, **kw):
         d = dict(k_flip=16, thr_accept_eq=42949672, thr_reduce=2147483648,
-                 thr_expand=42949672, expand_slack=2)
+                 thr_expand=42949672, expand_slack=2, mode=0)
         d.update(kw)
         return cls(**d)
 
@@ -48,6 +48,7 @@ class OracleParams(C.Structure):
 class _Walker(C.Structure):
     _fields_ = [("m", C.c_int), ("n", C.c_int), ("p", C.c_int), ("ring", C.c_int),
                 ("R", C.c_int), ("len", C.c_int * 3), ("r", C.c_int), ("best_r", C.c_int),
+                ("best_adds", C.c_int),
                 ("walker_id", C.c_uint64), ("step", C.c_uint64), ("digest", C.c_uint64),
                 ("cnt", C.c_uint64 * NCNT), ("rows", C.c_void_p), ("best", C.c_void_p)]
 
@@ -229,6 +230,10 @@ class OracleWalker:
     @property
     def digest(self):
         return self.w.digest
+
+    @property
+    def best_adds(self):
+        return self.w.best_adds
 
     @property
     def step(self):

@@ -152,7 +152,7 @@ static void flip_roles(int X, int e, int *Y, int *Z)
      = x (x) (y_a + s y_b) (x) z_a + s x (x) y_b (x) (z_b - z_a)
    Returns 1 and commits (then normalises rows alpha, beta) iff both new factors
    stay in Z_T. */
-static int flip_move(or_walker *w, const cand_t *c, int d, int e, int *alpha, int *beta)
+static int flip_move(or_walker *w, const cand_t *c, int d, int e, int nonzero, int *alpha, int *beta)
 {
     int Y, Z, al, be;
     int8_t ny[OR_MAXLEN], nz[OR_MAXLEN];
@@ -161,6 +161,7 @@ static int flip_move(or_walker *w, const cand_t *c, int d, int e, int *alpha, in
     be = d ? c->i : c->j;
     if (!vec_add(w->ring, ny, FAC(w, al, Y), FAC(w, be, Y), c->sigma, w->len[Y])) return 0;
     if (!vec_add(w->ring, nz, FAC(w, be, Z), FAC(w, al, Z), -1, w->len[Z])) return 0;
+    if (nonzero && (is_zero(ny, w->len[Y]) || is_zero(nz, w->len[Z]))) return 0;   /* R24 */
     memcpy(FAC(w, al, Y), ny, (size_t)w->len[Y]);
     memcpy(FAC(w, be, Z), nz, (size_t)w->len[Z]);
     normalize_row(w, al);
@@ -173,7 +174,7 @@ static int flip_move(or_walker *w, const cand_t *c, int d, int e, int *alpha, in
 /* R11 try_flip: up to K uniform draws over 4|C| (candidate x 2 orders x 2 role
    swaps); the list is not rebuilt between draws. */
 static int try_flip(or_walker *w, const cand_t *C, int nC, uint64_t seed, const or_params *prm,
-                    int *alpha, int *beta, int *draws)
+                    int nonzero, int *alpha, int *beta, int *draws)
 {
     uint32_t a;
     *draws = 0;
@@ -182,7 +183,7 @@ static int try_flip(or_walker *w, const cand_t *C, int nC, uint64_t seed, const 
         int slot = a == 0 ? 0 : 7 + (int)a;
         uint32_t k = uniform(word(w, seed, slot), 4u * (uint32_t)nC);
         (*draws)++;
-        if (flip_move(w, &C[k >> 2], (int)(k & 1), (int)((k >> 1) & 1), alpha, beta)) return 1;
+        if (flip_move(w, &C[k >> 2], (int)(k & 1), (int)((k >> 1) & 1), nonzero, alpha, beta)) return 1;
     }
     return 0;
 }
@@ -394,6 +395,60 @@ static void digest_mix(or_walker *w, uint64_t ev)
     w->digest ^= w->digest >> 32;
 }
 
+/* naive additions of the first `rank` rows of a row array */
+static int rows_additions(const or_walker *w, const int8_t *rows, int rank)
+{
+    int l, X, e, nnz = 0;
+    for (l = 0; l < rank; l++)
+        for (X = 0; X < 3; X++)
+            for (e = 0; e < w->len[X]; e++) nnz += rows[((size_t)l * 3 + X) * OR_MAXLEN + e] != 0;
+    return nnz - 2 * rank - w->m * w->p;
+}
+
+/* ---------- R24: one step of naive-complexity minimisation ----------
+   Random flips without reduction edges: try_flip (R11) where a draw is also
+   rejected if a new factor is zero; no local reduction, no reduce_all, no expand.
+   After a flip, the best scheme is replaced if (rank, additions) is smaller, or
+   equal with the 1% plateau acceptance (PAPER:310-313 applied to additions). */
+static void complexity_step(or_walker *w, uint64_t seed, const or_params *prm, cand_t *C, int8_t *vbuf)
+{
+    int nC, ok, alpha = 0, beta = 0, draws = 0;
+    uint32_t flags = 0;
+    uint64_t ev;
+    nC = build_candidates(w, C);
+    ok = try_flip(w, C, nC, seed, prm, 1, &alpha, &beta, &draws);
+    w->cnt[OR_C_DRAWS] += (uint64_t)draws;
+    if (!ok) {
+        w->cnt[OR_C_FLIP_FAIL]++;
+        alpha = beta = 0;
+    } else {
+        int adds = rows_additions(w, w->rows, w->r);
+        int better = w->r < w->best_r || (w->r == w->best_r && adds < w->best_adds);
+        w->cnt[OR_C_FLIPS]++;
+        flags |= EV_FLIP_OK;
+        if (better || (w->r == w->best_r && adds == w->best_adds && word(w, seed, 1) < prm->thr_accept_eq)) {
+            w->best_r = w->r;
+            w->best_adds = adds;
+            memcpy(w->best, w->rows, (size_t)w->r * 3 * OR_MAXLEN);
+            w->cnt[OR_C_BEST_COPIES]++;
+            flags |= EV_ACCEPT;
+            if (better) {
+                int32_t ff[3];
+                flags |= EV_STRICT;
+                w->cnt[OR_C_IMPROVEMENTS]++;
+                rows_to_coeffs(w, w->best, w->best_r, vbuf);
+                if (or_verify(w->m, w->n, w->p, w->ring, vbuf, w->best_r, ff) != 0)
+                    w->cnt[OR_C_VERIFY_FAIL]++;
+            }
+        }
+    }
+    ev = (uint64_t)(uint32_t)w->r | ((uint64_t)(uint32_t)(w->best_adds & 1023) << 10) |
+         ((uint64_t)flags << 20) | ((uint64_t)alpha << 32) | ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
+    digest_mix(w, ev);
+    w->cnt[OR_C_STEPS]++;
+    w->step++;
+}
+
 /* ---------- R17: one Alg.1 iteration ---------- */
 static void walk_step(or_walker *w, uint64_t seed, const or_params *prm, cand_t *C, int8_t *vbuf)
 {
@@ -401,7 +456,7 @@ static void walk_step(or_walker *w, uint64_t seed, const or_params *prm, cand_t 
     uint32_t flags = 0;
     uint64_t ev;
     nC = build_candidates(w, C);
-    ok = try_flip(w, C, nC, seed, prm, &alpha, &beta, &draws);
+    ok = try_flip(w, C, nC, seed, prm, 0, &alpha, &beta, &draws);
     w->cnt[OR_C_DRAWS] += (uint64_t)draws;
     if (!ok) {
         /* if not try_flip: expand; continue */
@@ -418,6 +473,7 @@ static void walk_step(or_walker *w, uint64_t seed, const or_params *prm, cand_t 
         if (w->r < w->best_r || (w->r == w->best_r && word(w, seed, 1) < prm->thr_accept_eq)) {
             int strict = w->r < w->best_r;
             w->best_r = w->r;
+            w->best_adds = rows_additions(w, w->rows, w->r);
             memcpy(w->best, w->rows, (size_t)w->r * 3 * OR_MAXLEN);
             w->cnt[OR_C_BEST_COPIES]++;
             flags |= EV_ACCEPT;
@@ -508,6 +564,7 @@ int or_seed_rows(or_walker *w, const int8_t *coeffs, int rank)
     if (rc) return rc;
     memcpy(w->best, w->rows, (size_t)(w->R + 1) * 3 * OR_MAXLEN);
     w->best_r = w->r;
+    w->best_adds = rows_additions(w, w->rows, w->r);
     w->step = 0;
     w->digest = DIGEST_INIT;
     memset(w->cnt, 0, sizeof(w->cnt));
@@ -532,7 +589,10 @@ void or_walk(or_walker *w, uint64_t steps, uint64_t seed, const or_params *prm)
     size_t maxc = (size_t)3 * w->R * (w->R + 1) / 2 + 1;
     cand_t *C = (cand_t *)malloc(maxc * sizeof(cand_t));
     int8_t *vbuf = (int8_t *)malloc((size_t)(w->R + 1) * (w->len[0] + w->len[1] + w->len[2]));
-    for (s = 0; s < steps; s++) walk_step(w, seed, prm, C, vbuf);
+    for (s = 0; s < steps; s++) {
+        if (prm->mode == 1) complexity_step(w, seed, prm, C, vbuf);
+        else walk_step(w, seed, prm, C, vbuf);
+    }
     free(C);
     free(vbuf);
 }
@@ -550,6 +610,7 @@ void or_restart(or_walker *w, const int8_t *coeffs, int rank)
     if (load_rows(w, coeffs, rank) != 0) return;
     memcpy(w->best, w->rows, (size_t)(w->R + 1) * 3 * OR_MAXLEN);
     w->best_r = w->r;
+    w->best_adds = rows_additions(w, w->rows, w->r);
     digest_mix(w, 0xA5A5000000000000ULL | (uint64_t)(uint32_t)rank);
 }
 
@@ -578,7 +639,7 @@ int or_apply_flip(or_walker *w, int cand, int d, int e)
     size_t maxc = (size_t)3 * w->R * (w->R + 1) / 2 + 1;
     cand_t *C = (cand_t *)malloc(maxc * sizeof(cand_t));
     int n = build_candidates(w, C), a, b, ok = 0;
-    if (cand >= 0 && cand < n) ok = flip_move(w, &C[cand], d, e, &a, &b);
+    if (cand >= 0 && cand < n) ok = flip_move(w, &C[cand], d, e, 0, &a, &b);
     free(C);
     return ok;
 }

@@ -235,6 +235,7 @@ int seed_planes(fg_ctx *c, const uint64_t *planes, int rank, int64_t w0, int64_t
     h.best_r = rank;
     h.step = 0;
     h.digest = 0xcbf29ce484222325ULL;
+    h.best_adds = additions_planes(c->m, c->p, planes, c->R, rank);
     uint64_t *tmp = nullptr;
     fg_whdr *tmph = nullptr;
     CK(cudaMallocAsync((void **)&tmp, words * sizeof(uint64_t), c->stream));
@@ -423,7 +424,8 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     if (!c->seeded) return FG_E_STATE;
     fg_params P;
     if (prm) P = *prm; else fg_params_default(&P);
-    if (P.k_flip < 1 || P.k_flip > 16 || P.flags != 0 || P.expand_slack < -FG_MAX_RCAP) return FG_E_ARG;
+    if (P.k_flip < 1 || P.k_flip > 16 || (P.flags & ~FG_FLAG_COMPLEXITY) || P.expand_slack < -FG_MAX_RCAP)
+        return FG_E_ARG;
     CK(cudaSetDevice(c->device));
     WalkArgs a;
     memset(&a, 0, sizeof(a));
@@ -432,6 +434,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.m = c->m; a.n = c->n; a.p = c->p; a.R = c->R;
     a.len_u = c->len[0]; a.len_v = c->len[1]; a.len_w = c->len[2]; a.mp = c->m * c->p;
     a.seed = seed;
+    a.mode = (P.flags & FG_FLAG_COMPLEXITY) ? 1u : 0u;
     a.k_flip = P.k_flip; a.thr_eq = P.thr_accept_eq; a.thr_reduce = P.thr_reduce;
     a.thr_expand = P.thr_expand; a.slack = P.expand_slack;
     a.q_planes = c->d_qplanes; a.q_meta = c->d_qmeta; a.q_count = &c->d_misc->q_count;
@@ -457,7 +460,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         CK(cudaMemsetAsync(&c->d_misc->q_count, 0, sizeof(uint32_t), c->stream));
         CK(cudaMemsetAsync(&c->d_misc->work_counter, 0, sizeof(unsigned long long), c->stream));
         CK(cudaEventRecord(c->ev0, c->stream));
-        CK(fg_launch_walk(c->kind, a, c->num_sms, c->stream));
+        CK(fg_launch_walk(a.mode ? fg_kind_for_mode(c->kind) : c->kind, a, c->num_sms, c->stream));
         CK(cudaEventRecord(c->ev1, c->stream));
         CK(fg_launch_verify(v, c->stream));
         CK(cudaEventRecord(c->ev2, c->stream));
@@ -476,6 +479,16 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     if (a.dbg && hm.dbgbuf[0])
         fprintf(stderr, "libfg dbg: %u %u %u %u %u %u %u %u %u %u\n", hm.dbgbuf[0], hm.dbgbuf[1], hm.dbgbuf[2],
                 hm.dbgbuf[3], hm.dbgbuf[4], hm.dbgbuf[5], hm.dbgbuf[6], hm.dbgbuf[7], hm.dbgbuf[8], hm.dbgbuf[9]);
+    if (hm.q_overflow) {
+        // strict improvements that missed the queue: verify those walkers' final bests
+        CK(cudaMemsetAsync(&c->d_misc->restarted, 0, sizeof(unsigned long long), c->stream));
+        CK(fg_launch_verify_flagged(c->d_best, c->d_hdr, c->W, c->R, c->m, c->n, c->p, c->ring,
+                                    &c->d_misc->verify_fail, &c->d_misc->restarted, c->stream));
+        c->st_launches++;
+        CK(cudaMemcpyAsync(&hm, c->d_misc, sizeof(hm), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        verified += hm.restarted;
+    }
     int rc = refresh_local_best(c, hm.best_key);
     if (rc != FG_OK) return rc;
     c->st_vfail += hm.verify_fail;
@@ -559,8 +572,8 @@ int fg_best(const fg_ctx *c, int *rank, int *adds, int64_t *walker_id, int8_t *c
     return FG_OK;
 }
 
-int fg_get_walkers(const fg_ctx *c, int64_t w0, int64_t w1, int32_t *r, int32_t *best_r, uint64_t *digest,
-                   uint64_t *step, uint64_t *cnt, int8_t *rows, int8_t *best)
+int fg_get_walkers(const fg_ctx *c, int64_t w0, int64_t w1, int32_t *r, int32_t *best_r, int32_t *best_adds,
+                   uint64_t *digest, uint64_t *step, uint64_t *cnt, int8_t *rows, int8_t *best)
 {
     if (!c || w0 < 0 || w1 > c->W || w0 > w1) return FG_E_ARG;
     if (w0 == w1) return FG_OK;
@@ -583,6 +596,7 @@ int fg_get_walkers(const fg_ctx *c, int64_t w0, int64_t w1, int32_t *r, int32_t 
     for (int64_t k = 0; k < nw; ++k) {
         if (r) r[k] = h[k].r;
         if (best_r) best_r[k] = h[k].best_r;
+        if (best_adds) best_adds[k] = h[k].best_adds;
         if (digest) digest[k] = h[k].digest;
         if (step) step[k] = h[k].step;
         if (cnt) memcpy(cnt + k * FG_NCNT, h[k].cnt, sizeof(uint64_t) * FG_NCNT);
@@ -604,7 +618,7 @@ int fg_get_walker(const fg_ctx *c, int64_t wk, int *rank, int *best_rank, uint64
                   int8_t *coeffs_out, int8_t *best_out)
 {
     int32_t r = 0, br = 0;
-    int rc = fg_get_walkers(c, wk, wk + 1, &r, &br, digest, nullptr, nullptr, coeffs_out, best_out);
+    int rc = fg_get_walkers(c, wk, wk + 1, &r, &br, nullptr, digest, nullptr, nullptr, coeffs_out, best_out);
     if (rc != FG_OK) return rc;
     if (rank) *rank = r;
     if (best_rank) *best_rank = br;
@@ -714,7 +728,7 @@ int fg_restart(fg_ctx *c, int slack, int64_t *restarted)
     const size_t words = (size_t)FG_PLANES * c->R;
     CK(cudaMemcpyAsync(c->d_pool, (const uint64_t *)(b + 1), words * 8, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemsetAsync(&c->d_misc->restarted, 0, sizeof(unsigned long long), c->stream));
-    CK(fg_launch_restart(c->d_cur, c->d_best, c->d_hdr, c->W, c->R, c->d_pool, b->rank, slack,
+    CK(fg_launch_restart(c->d_cur, c->d_best, c->d_hdr, c->W, c->R, c->d_pool, b->rank, b->additions, slack,
                          &c->d_misc->restarted, c->stream));
     c->st_launches++;
     unsigned long long n = 0;

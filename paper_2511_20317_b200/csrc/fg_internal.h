@@ -18,7 +18,8 @@ struct __align__(16) fg_whdr {     // per-walker header, 128 B
     uint64_t step;                 // Alg.1 iteration index since seeding (R8)
     uint64_t digest;
     uint64_t cnt[FG_NCNT];
-    uint64_t pad;
+    int32_t best_adds;             // naive additions of the best scheme
+    int32_t pad;                   // bit 0: a strict improvement missed the verify queue
 };
 static_assert(sizeof(fg_whdr) == 128, "fg_whdr size");
 
@@ -57,6 +58,7 @@ struct WalkArgs {
     // local best key (R20): rank<<54 | additions<<36 | local walker index
     unsigned long long *best_key;
     unsigned long long *work_counter;   // dynamic walker queue, zeroed before each launch
+    uint32_t mode;                      // 0 = Alg. 1 walk, 1 = naive-complexity minimisation (R24)
     uint32_t dbg;                       // debug switches (env FG_DBG), 0 in production
     uint32_t *dbgbuf;                   // 16 words of debug output (first error wins)
 };
@@ -85,7 +87,11 @@ const char *fg_kernel_kind_name(int kind);
 cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 cudaError_t fg_launch_verify(const VerifyArgs &a, cudaStream_t st);
 cudaError_t fg_launch_restart(uint64_t *cur, uint64_t *best, fg_whdr *hdr, int64_t num_walkers,
-                              int R, const uint64_t *pool_planes, int pool_rank, int slack,
+                              int R, const uint64_t *pool_planes, int pool_rank, int pool_adds, int slack,
                               unsigned long long *restarted, cudaStream_t st);
+int fg_kind_for_mode(int kind);
+cudaError_t fg_launch_verify_flagged(const uint64_t *best, fg_whdr *hdr, int64_t num_walkers, int R, int m,
+                                     int n, int p, int ring, uint32_t *fail_count, unsigned long long *done,
+                                     cudaStream_t st);   // R24 runs on the one-walker-per-warp / multi-row kernels
 cudaError_t fg_launch_bestkey(const uint64_t *best, const fg_whdr *hdr, int64_t num_walkers, int R, int mp,
                               unsigned long long *key, cudaStream_t st);

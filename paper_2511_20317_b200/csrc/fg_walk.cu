@@ -82,7 +82,11 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
         int best = hp->best_r;
         uint64_t step = hp->step;
         uint64_t digest = hp->digest;
+        int best_adds = hp->best_adds;
         const uint32_t wid = (uint32_t)(a.id_base + wk);
+        const bool cmode = a.mode == 1;          // R24: naive-complexity minimisation
+        // nnz of the current scheme (additions = nnz - 2r - mp), tracked in R24 mode
+        int nnz_cur = __reduce_add_sync(FULL, lane < r ? P::popd(row.u) + P::popd(row.v) + P::popd(row.w) : 0);
 
         uint32_t c_draws = 0, c_flips = 0, c_red = 0;
         if (lane < 8) rc[lane] = 0;
@@ -259,6 +263,37 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
             return true;
         };
 
+        // best copy to HBM and the R19 verify queue
+        auto store_rows = [&](uint64_t *dst) {
+            if (lane < R) {
+                const bool lv = lane < r;
+                dst[0 * R + lane] = lv ? P::dig(row.u) : 0;
+                dst[1 * R + lane] = lv ? P::sgn(row.u) : 0;
+                dst[2 * R + lane] = lv ? P::dig(row.v) : 0;
+                dst[3 * R + lane] = lv ? P::sgn(row.v) : 0;
+                dst[4 * R + lane] = lv ? P::dig(row.w) : 0;
+                dst[5 * R + lane] = lv ? P::sgn(row.w) : 0;
+            }
+        };
+        auto store_best = [&]() { store_rows(bw); };
+        auto enqueue_verify = [&]() {
+            unsigned slot = 0;
+            if (lane == 0) slot = atomicAdd(a.q_count, 1u);
+            slot = __shfl_sync(FULL, slot, 0);
+            if (slot < a.q_cap) {
+                store_rows(a.q_planes + (size_t)slot * FG_PLANES * R);
+                if (lane == 0) {
+                    fg_qmeta qm;
+                    qm.walker = wk; qm.step = step; qm.rank = r; qm.ok = -1;
+                    qm.ff[0] = qm.ff[1] = qm.ff[2] = -1; qm.pad = 0;
+                    a.q_meta[slot] = qm;
+                }
+            } else if (lane == 0) {
+                atomicAdd(a.q_overflow, 1u);
+                hp->pad |= 1;
+            }
+        };
+
         compute_masks();
         int boff = 32;
 
@@ -339,6 +374,8 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 e_ny = P::add(get(ra, Y), P::sel(sneg, P::neg(yb), yb), v);     // y_a + s y_b
                 e_nz = P::sub(get(rb, Z), get(ra, Z), v);              // z_b - z_a
                 e_al = al; e_be = be; e_Y = Y; e_Z = Z;
+                // R24: no reduction edges -> a draw making a factor zero is rejected
+                if (cmode) v = v && !P::zero(e_ny) && !P::zero(e_nz);
                 return v;
             };
 
@@ -369,9 +406,15 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                     const F nz = P::shfl(e_nz, src);
                     alpha = info & 255;
                     beta = (info >> 8) & 255;
+                    const bool touched = lane == alpha || lane == beta;
+                    const int pold = touched ? P::popd(row.u) + P::popd(row.v) + P::popd(row.w) : 0;
                     set(row, (info >> 16) & 3, ny, lane == alpha);
                     set(row, (info >> 18) & 3, nz, lane == beta);
-                    if (lane == alpha || lane == beta) normalize<P>(row);
+                    if (touched) normalize<P>(row);
+                    if (cmode) {
+                        const int pnew = touched ? P::popd(row.u) + P::popd(row.v) + P::popd(row.w) : 0;
+                        nnz_cur += __reduce_add_sync(FULL, pnew - pold);
+                    }
                     ok = true;
                 } else {
                     draws = kf;
@@ -379,7 +422,28 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
             }
             c_draws += draws;
 
-            if (!ok) {
+            if (cmode) {
+                // ---- R24 step: flips only; best by (rank, naive additions) ----
+                if (ok) {
+                    c_flips++;
+                    flags |= 1u;
+                    update_masks2(alpha, beta);
+                    const int adds = nnz_cur - 2 * r - a.mp;
+                    const bool better = r < best || (r == best && adds < best_adds);
+                    if (better || (r == best && adds == best_adds && (bern & 1u))) {
+                        best = r;
+                        best_adds = adds;
+                        bump(RC_COPY, 1);
+                        flags |= 4u;
+                        store_best();
+                        if (better) {
+                            flags |= 8u;
+                            bump(RC_IMPR, 1);
+                            enqueue_verify();
+                        }
+                    }
+                }
+            } else if (!ok) {
                 // expand; continue
                 const bool ex = expand();
                 bump(RC_EOK, ex);
@@ -404,44 +468,15 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 if (acc) {
                     const bool strict = r < best;
                     best = r;
+                    best_adds = __reduce_add_sync(FULL, lane < r ? P::popd(row.u) + P::popd(row.v) + P::popd(row.w) : 0) -
+                                2 * r - a.mp;
                     bump(RC_COPY, 1);
                     flags |= 4u;
-                    if (lane < R) {
-                        const bool lv = lane < r;
-                        bw[0 * R + lane] = lv ? P::dig(row.u) : 0;
-                        bw[1 * R + lane] = lv ? P::sgn(row.u) : 0;
-                        bw[2 * R + lane] = lv ? P::dig(row.v) : 0;
-                        bw[3 * R + lane] = lv ? P::sgn(row.v) : 0;
-                        bw[4 * R + lane] = lv ? P::dig(row.w) : 0;
-                        bw[5 * R + lane] = lv ? P::sgn(row.w) : 0;
-                    }
+                    store_best();
                     if (strict) {
                         flags |= 8u;
                         bump(RC_IMPR, 1);
-                        // R19: enqueue for the batched Brent verifier
-                        unsigned slot = 0;
-                        if (lane == 0) slot = atomicAdd(a.q_count, 1u);
-                        slot = __shfl_sync(FULL, slot, 0);
-                        if (slot < a.q_cap) {
-                            uint64_t *qp = a.q_planes + (size_t)slot * FG_PLANES * R;
-                            if (lane < R) {
-                                const bool lv = lane < r;
-                                qp[0 * R + lane] = lv ? P::dig(row.u) : 0;
-                                qp[1 * R + lane] = lv ? P::sgn(row.u) : 0;
-                                qp[2 * R + lane] = lv ? P::dig(row.v) : 0;
-                                qp[3 * R + lane] = lv ? P::sgn(row.v) : 0;
-                                qp[4 * R + lane] = lv ? P::dig(row.w) : 0;
-                                qp[5 * R + lane] = lv ? P::sgn(row.w) : 0;
-                            }
-                            if (lane == 0) {
-                                fg_qmeta qm;
-                                qm.walker = wk; qm.step = step; qm.rank = r; qm.ok = -1;
-                                qm.ff[0] = qm.ff[1] = qm.ff[2] = -1; qm.pad = 0;
-                                a.q_meta[slot] = qm;
-                            }
-                        } else if (lane == 0) {
-                            atomicAdd(a.q_overflow, 1u);
-                        }
+                        enqueue_verify();
                     }
                 }
                 // ---- PAPER:315-317 reduce (R15) ----
@@ -463,7 +498,7 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
                 }
             }
             // ---- digest ----
-            const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)best << 10) |
+            const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)(cmode ? (best_adds & 1023) : best) << 10) |
                                 ((uint64_t)flags << 20) | ((uint64_t)alpha << 32) |
                                 ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
             digest = (digest ^ ev) * 0x100000001b3ULL;
@@ -489,6 +524,7 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
             hp->best_r = best;
             hp->step = step;
             hp->digest = digest;
+            hp->best_adds = best_adds;
             hp->cnt[FG_CNT_STEPS] += a.steps;
             hp->cnt[FG_CNT_DRAWS] += c_draws;
             hp->cnt[FG_CNT_FLIPS] += c_flips;
@@ -548,6 +584,16 @@ int fg_pick_kernel(int ring, int maxlen, int R)
         return w32 ? FG_K_W32_Z2_K32 : FG_K_H16_Z2;
     }
     return fg_multi_kind(ring, maxlen, R);
+}
+
+int fg_kind_for_mode(int kind)
+{
+    switch (kind) {
+    case FG_K_H16_P16: return FG_K_W32_ZT_K16;
+    case FG_K_H16_P32: return FG_K_W32_ZT_K32;
+    case FG_K_H16_Z2: return FG_K_W32_Z2_K32;
+    default: return kind;
+    }
 }
 
 const char *fg_kernel_kind_name(int kind)

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(H16_THREADS, H16_MINB) walk_h16(WalkArgs a)
         int best = act ? hp->best_r : 0;
         uint64_t step = act ? hp->step : 0;
         uint64_t digest = act ? hp->digest : 0;
+        int best_adds = act ? hp->best_adds : 0;
         const uint32_t wid = (uint32_t)(a.id_base + (act ? wk : 0));
         uint32_t c_draws = 0, c_flips = 0, c_red = 0;
         enum { RC_EOK = 0, RC_EREJ, RC_MERGE, RC_ZERO, RC_COPY, RC_IMPR };
@@ -529,8 +530,16 @@ __global__ void __launch_bounds__(H16_THREADS, H16_MINB) walk_h16(WalkArgs a)
                     unsigned slot = 0;
                     if (k == 0 && strict) slot = atomicAdd(a.q_count, 1u);
                     slot = __shfl_sync(FULL, slot, hb);
+                    int nz = 0;
+                    if (acc) {
+                        nz = (k < r ? P::popd(row0.u) + P::popd(row0.v) + P::popd(row0.w) : 0) +
+                             (16 + k < r ? P::popd(row1.u) + P::popd(row1.v) + P::popd(row1.w) : 0);
+                    }
+#pragma unroll
+                    for (int o = 8; o >= 1; o >>= 1) nz += __shfl_xor_sync(FULL, nz, o, 16);
                     if (acc) {
                         best = r;
+                        best_adds = nz - 2 * r - a.mp;
                         bump(RC_COPY, 1);
                         flags |= 4u;
                         store_rows(bw);
@@ -547,6 +556,7 @@ __global__ void __launch_bounds__(H16_THREADS, H16_MINB) walk_h16(WalkArgs a)
                                 }
                             } else if (k == 0) {
                                 atomicAdd(a.q_overflow, 1u);
+                                hp->pad |= 1;
                             }
                         }
                     }
@@ -630,6 +640,7 @@ __global__ void __launch_bounds__(H16_THREADS, H16_MINB) walk_h16(WalkArgs a)
             hp->best_r = best;
             hp->step = step;
             hp->digest = digest;
+            hp->best_adds = best_adds;
             hp->cnt[FG_CNT_STEPS] += a.steps;
             hp->cnt[FG_CNT_DRAWS] += c_draws;
             hp->cnt[FG_CNT_FLIPS] += c_flips;

@@ -72,7 +72,9 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
         int best = hp->best_r;
         uint64_t step = hp->step;
         uint64_t digest = hp->digest;
+        int best_adds = hp->best_adds;
         const uint32_t wid = (uint32_t)(a.id_base + wk);
+        const bool cmode = a.mode == 1;          // R24: naive-complexity minimisation
         uint32_t c_draws = 0, c_flips = 0, c_red = 0;
         enum { RC_EOK = 0, RC_EREJ, RC_MERGE, RC_ZERO, RC_COPY, RC_IMPR };
         auto bump = [&](int k, uint32_t v) { if (lane == 0) rc[k] += v; };
@@ -419,7 +421,16 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
             }
         };
 
+        auto nnz_all = [&]() -> int {
+            int v = 0;
+#pragma unroll
+            for (int s = 0; s < NS; ++s)
+                if (lane * NS + s < r) v += P::popd(own(0, s)) + P::popd(own(1, s)) + P::popd(own(2, s));
+            return __reduce_add_sync(FULL, v);
+        };
+        auto popr = [&](const Row<P> &x) { return P::popd(x.u) + P::popd(x.v) + P::popd(x.w); };
         recount();
+        int nnz_cur = nnz_all();
         int boff = 32;
         const uint32_t nsteps = (uint32_t)a.steps;
         for (uint32_t it = 0; it < nsteps; ++it, ++step, ++boff) {
@@ -529,6 +540,8 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     const F yb = get(rb, Y);
                     const F ny = P::add(get(ra, Y), P::sel(sneg, P::neg(yb), yb), v);
                     const F nz = P::sub(get(rb, Z), get(ra, Z), v);
+                    // R24: no reduction edges -> a draw making a factor zero is rejected
+                    if (cmode) v = v && !P::zero(ny) && !P::zero(nz);
                     if (!v) continue;
                     Row<P> na = ra, nb = rb;
                     set(na, Y, ny, true);
@@ -537,6 +550,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     normalize<P>(nb);
                     put_row(al, na);
                     put_row(be, nb);
+                    if (cmode) nnz_cur += popr(na) + popr(nb) - popr(ra) - popr(rb);
                     alpha = al;
                     beta = be;
                     ok = true;
@@ -545,7 +559,41 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
             }
             c_draws += draws;
 
-            if (!ok) {
+            if (cmode) {
+                // ---- R24 step: flips only; best by (rank, naive additions) ----
+                if (ok) {
+                    c_flips++;
+                    flags |= 1u;
+                    const int adds = nnz_cur - 2 * r - a.mp;
+                    const bool better = r < best || (r == best && adds < best_adds);
+                    if (better || (r == best && adds == best_adds && (bern & 1u))) {
+                        best = r;
+                        best_adds = adds;
+                        bump(RC_COPY, 1);
+                        flags |= 4u;
+                        store_rows(bw);
+                        if (better) {
+                            flags |= 8u;
+                            bump(RC_IMPR, 1);
+                            unsigned slot = 0;
+                            if (lane == 0) slot = atomicAdd(a.q_count, 1u);
+                            slot = __shfl_sync(FULL, slot, 0);
+                            if (slot < a.q_cap) {
+                                store_rows(a.q_planes + (size_t)slot * FG_PLANES * R);
+                                if (lane == 0) {
+                                    fg_qmeta qm;
+                                    qm.walker = wk; qm.step = step; qm.rank = r; qm.ok = -1;
+                                    qm.ff[0] = qm.ff[1] = qm.ff[2] = -1; qm.pad = 0;
+                                    a.q_meta[slot] = qm;
+                                }
+                            } else if (lane == 0) {
+                                atomicAdd(a.q_overflow, 1u);
+                                hp->pad |= 1;
+                            }
+                        }
+                    }
+                }
+            } else if (!ok) {
                 const bool ex = expand();
                 bump(RC_EOK, ex);
                 bump(RC_EREJ, !ex);
@@ -580,6 +628,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                 if (acc) {
                     const bool strict = r < best;
                     best = r;
+                    best_adds = nnz_all() - 2 * r - a.mp;
                     bump(RC_COPY, 1);
                     flags |= 4u;
                     store_rows(bw);
@@ -599,6 +648,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                             }
                         } else if (lane == 0) {
                             atomicAdd(a.q_overflow, 1u);
+                            hp->pad |= 1;
                         }
                     }
                 }
@@ -616,7 +666,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     bump(RC_EREJ, !ex);
                 }
             }
-            const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)best << 10) |
+            const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)(cmode ? (best_adds & 1023) : best) << 10) |
                                 ((uint64_t)flags << 20) | ((uint64_t)alpha << 32) |
                                 ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
             digest = (digest ^ ev) * 0x100000001b3ULL;
@@ -636,6 +686,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
             hp->best_r = best;
             hp->step = step;
             hp->digest = digest;
+            hp->best_adds = best_adds;
             hp->cnt[FG_CNT_STEPS] += a.steps;
             hp->cnt[FG_CNT_DRAWS] += c_draws;
             hp->cnt[FG_CNT_FLIPS] += c_flips;

@@ -13,6 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIBFG = os.path.join(HERE, "libfg.so")
 
 FG_ZT, FG_Z2 = 0, 1
+FG_FLAG_COMPLEXITY = 1
 FG_NCNT = 12
 CNT_NAMES = ["steps", "draws", "flips", "flip_fail", "expand_ok", "expand_reject", "merges",
              "zero_removed", "best_copies", "improvements", "reduce_calls", "verify_fail"]
@@ -54,7 +55,7 @@ _sig = {
     "fg_verify": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
     "fg_verify_batch": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "fg_best": (_i32, [_vp, _vp, _vp, _vp, _vp]),
-    "fg_get_walkers": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fg_get_walkers": (_i32, [_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fg_get_walker": (_i32, [_vp, _i64, _vp, _vp, _vp, _vp, _vp]),
     "fg_record_bytes": (_sz, [_i32]),
     "fg_export_best": (_i32, [_vp, _vp]),
@@ -211,14 +212,15 @@ class FlipGraph:
         k = w_end - w_begin
         r = np.zeros(k, np.int32)
         br = np.zeros(k, np.int32)
+        ba = np.zeros(k, np.int32)
         dg = np.zeros(k, np.uint64)
         st = np.zeros(k, np.uint64)
         cnt = np.zeros((k, FG_NCNT), np.uint64)
         cur = np.zeros((k, self.R, self.width), np.int8) if rows else None
         best = np.zeros((k, self.R, self.width), np.int8) if rows else None
-        _ck(_lib.fg_get_walkers(self.ctx, w_begin, w_end, _p(r), _p(br), _p(dg), _p(st), _p(cnt),
-                                _p(cur), _p(best)), "fg_get_walkers")
-        return dict(r=r, best_r=br, digest=dg, step=st, cnt=cnt, rows=cur, best=best)
+        _ck(_lib.fg_get_walkers(self.ctx, w_begin, w_end, _p(r), _p(br), _p(ba), _p(dg), _p(st),
+                                _p(cnt), _p(cur), _p(best)), "fg_get_walkers")
+        return dict(r=r, best_r=br, best_adds=ba, digest=dg, step=st, cnt=cnt, rows=cur, best=best)
 
     def record_bytes(self):
         return fg_record_bytes(self.R)

@@ -261,3 +261,46 @@ def test_multi_row_seeded_pool_and_restart(fg, orc):
     got = g.get_walkers()
     ref = orc.run_walkers(2, 2, 2, ZT, 40, 20, 3, 800, 11, seed_coeffs=strassen)
     _assert_same(got, ref, what="multi seed_pool")
+
+
+# ---------------- R24 naive-complexity minimisation ----------------
+@pytest.mark.parametrize("case", [((3, 3, 3), ZT, 32, 256), ((3, 3, 3), Z2, 32, 128),
+                                  ((4, 4, 4), ZT, 96, 64), ((2, 3, 4), ZT, 32, 96)],
+                         ids=lambda c: f"{c[0]}-{'ZT' if c[1] == 0 else 'Z2'}-R{c[2]}")
+def test_complexity_mode_parity(fg, orc, case):
+    """Seed every walker with a walked (dense) scheme, run R24 on the GPU and in the
+    oracle: trajectories bit-exact; best additions only fall; rank constant."""
+    (m, n, p), ring, R, W = case
+    w = orc.walker(m, n, p, ring, R, walker_id=5)
+    w.seed_naive()
+    w.walk(6000, 99)
+    start = w.rows(0)
+    a0 = orc.additions(m, n, p, start)
+    g = _ctx(fg, m, n, p, ring, R, W, base=11)
+    g.seed_pool(start)
+    prm = fg.params_default(flags=fg.FG_FLAG_COMPLEXITY)
+    g.walk(1500, 4242, prm)
+    got = g.get_walkers()
+    ids = sample_walkers(W, 16, seed=5)
+    ref = orc.run_walkers(m, n, p, ring, R, 0, 0, 1500, 4242, seed_coeffs=start,
+                          params=OracleParams.default(mode=1), ids=ids + 11)
+    _assert_same(got, ref, idx=ids, what=f"R24 {(m, n, p)}")
+    assert np.all(got["r"] == start.shape[0])
+    for k in range(W):
+        b = got["best"][k][: got["best_r"][k]]
+        assert got["best_adds"][k] == orc.additions(m, n, p, b) <= a0
+    st = g.stats()
+    # improvements are frequent in R24: those that overflow the queue are covered by
+    # verifying the walker's final best (DESIGN.md section 4)
+    assert st["verify_fail"] == 0 and st["verified"] > 0
+    bb = g.best()
+    assert bb["additions"] == int(got["best_adds"].min()) and fg.fg_verify(m, n, p, ring, bb["coeffs"])[0] == 0
+
+
+def test_best_adds_tracks_best_scheme_in_walk_mode(fg, orc):
+    g = _ctx(fg, 3, 3, 3, ZT, 32, 512)
+    g.seed_naive()
+    g.walk(5000, 21)
+    got = g.get_walkers()
+    for k in range(0, 512, 5):
+        assert got["best_adds"][k] == orc.additions(3, 3, 3, got["best"][k][: got["best_r"][k]])
