@@ -45,7 +45,7 @@ __device__ __forceinline__ int nth_bit(uint32_t x, uint32_t t)
     return __ffs(x) - 1;
 }
 
-template <class P>
+template <class P, bool CM>
 __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
 {
     typedef typename P::F F;
@@ -84,9 +84,9 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
         uint64_t digest = hp->digest;
         int best_adds = hp->best_adds;
         const uint32_t wid = (uint32_t)(a.id_base + wk);
-        const bool cmode = a.mode == 1;          // R24: naive-complexity minimisation
+        constexpr bool cmode = CM;               // R24: naive-complexity minimisation
         // nnz of the current scheme (additions = nnz - 2r - mp), tracked in R24 mode
-        int nnz_cur = __reduce_add_sync(FULL, lane < r ? P::popd(row.u) + P::popd(row.v) + P::popd(row.w) : 0);
+        int nnz_cur = CM ? __reduce_add_sync(FULL, lane < r ? P::popd(row.u) + P::popd(row.v) + P::popd(row.w) : 0) : 0;
 
         uint32_t c_draws = 0, c_flips = 0, c_red = 0;
         if (lane < 8) rc[lane] = 0;
@@ -547,11 +547,11 @@ __global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
     }
 }
 
-template <class P>
-cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
+template <class P, bool CM>
+cudaError_t launch_w32_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     int bps = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_w32<P>, W32_THREADS, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_w32<P, CM>, W32_THREADS, 0);
     if (e != cudaSuccess) return e;
     if (bps < 1) bps = 1;
     const int64_t wpb = W32_WARPS;
@@ -559,8 +559,14 @@ cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
     int64_t blocks = (int64_t)num_sms * bps;
     const int64_t need = (a.num_walkers + wpb - 1) / wpb;
     if (blocks > need) blocks = need;
-    walk_w32<P><<<(unsigned)blocks, W32_THREADS, 0, st>>>(a);
+    walk_w32<P, CM><<<(unsigned)blocks, W32_THREADS, 0, st>>>(a);
     return cudaGetLastError();
+}
+
+template <class P>
+cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
+{
+    return a.mode == 1 ? launch_w32_m<P, true>(a, num_sms, st) : launch_w32_m<P, false>(a, num_sms, st);
 }
 
 }  // namespace

@@ -27,7 +27,7 @@ using namespace fgd;
 
 namespace fgwm {
 
-template <class P, int NS>
+template <class P, int NS, bool CM>
 __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
 {
     typedef typename P::F F;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
         uint64_t digest = hp->digest;
         int best_adds = hp->best_adds;
         const uint32_t wid = (uint32_t)(a.id_base + wk);
-        const bool cmode = a.mode == 1;          // R24: naive-complexity minimisation
+        constexpr bool cmode = CM;               // R24: naive-complexity minimisation
         uint32_t c_draws = 0, c_flips = 0, c_red = 0;
         enum { RC_EOK = 0, RC_EREJ, RC_MERGE, RC_ZERO, RC_COPY, RC_IMPR };
         auto bump = [&](int k, uint32_t v) { if (lane == 0) rc[k] += v; };
@@ -708,18 +708,24 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
     }
 }
 
-template <class P, int NS>
-cudaError_t launch_wm(const WalkArgs &a, int num_sms, cudaStream_t st)
+template <class P, int NS, bool CM>
+cudaError_t launch_wm_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     const size_t smem = 3 * NS * 32 * sizeof(typename P::F) + 32 * PXS * 4 + 8 * 4;
     int bps = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_wm<P, NS>, 32, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_wm<P, NS, CM>, 32, smem);
     if (e != cudaSuccess) return e;
     if (bps < 1) bps = 1;
     int64_t blocks = (int64_t)num_sms * bps;
     if (blocks > a.num_walkers) blocks = a.num_walkers;
-    walk_wm<P, NS><<<(unsigned)blocks, 32, smem, st>>>(a);
+    walk_wm<P, NS, CM><<<(unsigned)blocks, 32, smem, st>>>(a);
     return cudaGetLastError();
+}
+
+template <class P, int NS>
+cudaError_t launch_wm(const WalkArgs &a, int num_sms, cudaStream_t st)
+{
+    return a.mode == 1 ? launch_wm_m<P, NS, true>(a, num_sms, st) : launch_wm_m<P, NS, false>(a, num_sms, st);
 }
 
 }  // namespace fgwm
