@@ -185,6 +185,33 @@ int fg_load_state(fg_ctx *ctx, const void *host_buf);
    [10] verify kernel ms (x1000), [11] walk launches.  out must hold 12. */
 int fg_stats(const fg_ctx *ctx, uint64_t out[12]);
 
+/* ---- Meta operators (section 3.3.2; readings R25-R30 in DESIGN.md) ----
+   Host only (no GPU), the orchestration between walks: schemes in the interchange
+   layout in and out, output rows NOT sign-normalised (fg_seed_pool normalises).
+   The caller sizes `out` for the result rank stated per function; the result
+   format must satisfy R1 (else FG_E_CAPACITY).  Errors as fg_verify.             */
+/* C = AB <=> C^T = B^T A^T: (m,n,p:r) -> (p,n,m:r) */
+int fg_meta_transpose(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out);
+/* cyclic symmetry of the matmul tensor: (u,v,w) -> (v,w,u), (m,n,p:r) -> (n,p,m:r) */
+int fg_meta_rotate(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out);
+/* swap sizes: (m,n,p:r) -> (m,p,n:r) = rotate(rotate(transpose)) */
+int fg_meta_swap_sizes(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out);
+/* project: (m,n,p) -> (m,n,p-1), drop the last column of B and C and the
+   terms left with a zero factor; *rank_out <= rank rows written */
+int fg_meta_project(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out, int *rank_out);
+/* extend: (m,n,p:r) -> (m,n,p+1 : r+mn), a naive (m,n,1) block appended */
+int fg_meta_extend(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out, int *rank_out);
+/* merge: (m,n,p1:ra) + (m,n,p2:rb) -> (m,n,p1+p2 : ra+rb), B = [B1 | B2] */
+int fg_meta_merge(int m, int n, int p1, int p2, int ring, const int8_t *a, int ra, const int8_t *b, int rb,
+                  int8_t *out);
+/* double: merge with itself, (m,n,p:r) -> (m,n,2p:2r) */
+int fg_meta_double(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out);
+/* product: Kronecker, (m1,n1,p1:ra) x (m2,n2,p2:rb) -> (m1m2,n1n2,p1p2 : ra*rb),
+   block index i = i1*m2 + i2 (same for j, k), row l = l1*rb + l2.  Block matrix
+   multiplication with Strassen is the product with a (2,2,2:7) scheme. */
+int fg_meta_product(int m1, int n1, int p1, const int8_t *a, int ra, int m2, int n2, int p2, const int8_t *b,
+                    int rb, int ring, int8_t *out);
+
 /* Which kernel variant fg_walk uses for this ctx ("warp32_zt_u32k", ...). */
 const char *fg_kernel_name(const fg_ctx *ctx);
 

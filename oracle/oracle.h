@@ -112,6 +112,16 @@ int  or_apply_expand(or_walker *w, int plus, int i, int j, int perm); /* 1 = app
 void or_reduce_all_public(or_walker *w);
 void or_local_reduce_public(or_walker *w, int a, int b);
 
+/* --- meta operators, meta.c: int8 rows in and out, not normalised --- */
+int or_meta_transpose(int m, int n, int p, const int8_t *in, int rank, int8_t *out);   /* -> (p,n,m) */
+int or_meta_rotate(int m, int n, int p, const int8_t *in, int rank, int8_t *out);      /* -> (n,p,m) */
+int or_meta_swap_sizes(int m, int n, int p, const int8_t *in, int rank, int8_t *out);  /* -> (m,p,n) */
+int or_meta_project(int m, int n, int p, const int8_t *in, int rank, int8_t *out, int *rank_out);
+int or_meta_extend(int m, int n, int p, const int8_t *in, int rank, int8_t *out, int *rank_out);
+int or_meta_merge(int m, int n, int p1, int p2, const int8_t *a, int ra, const int8_t *b, int rb, int8_t *out);
+int or_meta_product(int m1, int n1, int p1, const int8_t *a, int ra, int m2, int n2, int p2, const int8_t *b,
+                    int rb, int8_t *out);
+
 /* many walkers in one flat call (bench cpu baseline / tests): walker k has global
    id id_base+k, all seeded naive (or from coeffs if rank>0).  Output per walker:
    r, best_r, digest, cnt[OR_NCNT], and optionally rows/best (R*(mn+np+pm) int8). */

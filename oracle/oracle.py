@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
-SOURCES = ["philox_bits.c", "scheme.c", "walk.c"]
+SOURCES = ["philox_bits.c", "scheme.c", "walk.c", "meta.c"]
 NCNT = 12
 CNT_NAMES = ["steps", "draws", "flips", "flip_fail", "expand_ok", "expand_reject", "merges",
              "zero_removed", "best_copies", "improvements", "reduce_calls", "verify_fail"]
@@ -88,6 +88,12 @@ class Oracle:
         lib.or_apply_expand.argtypes = [vp, i32, i32, i32, i32]
         lib.or_reduce_all_public.argtypes = [vp]
         lib.or_local_reduce_public.argtypes = [vp, i32, i32]
+        for nm in ("or_meta_transpose", "or_meta_rotate", "or_meta_swap_sizes"):
+            getattr(lib, nm).argtypes = [i32, i32, i32, vp, i32, vp]
+        lib.or_meta_project.argtypes = [i32, i32, i32, vp, i32, vp, vp]
+        lib.or_meta_extend.argtypes = [i32, i32, i32, vp, i32, vp, vp]
+        lib.or_meta_merge.argtypes = [i32, i32, i32, i32, vp, i32, vp, i32, vp]
+        lib.or_meta_product.argtypes = [i32, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]
         lib.or_run_walkers.argtypes = [i32, i32, i32, i32, i32, i64, u64, vp, vp, i32, u64, u64,
                                        vp, i32, vp, vp, vp, vp, vp, vp]
 
@@ -145,6 +151,46 @@ class Oracle:
             rv, rw = divmod(rest, 65)
             res[(ru, rv, rw)] = int(out[idx])
         return res
+
+    # ---- meta operators: return ((m, n, p), coeffs) ----
+    def meta(self, op, fmt, coeffs, fmt2=None, coeffs2=None):
+        m, n, p = fmt
+        c = np.ascontiguousarray(coeffs, dtype=np.int8)
+        r = c.shape[0]
+        rk = C.c_int(0)
+        if op in ("transpose", "rotate", "swap_sizes"):
+            nf = {"transpose": (p, n, m), "rotate": (n, p, m), "swap_sizes": (m, p, n)}[op]
+            out = np.zeros((r, c.shape[1]), np.int8)
+            rc = getattr(self.lib, "or_meta_" + op)(m, n, p, _p(c), r, _p(out))
+        elif op == "project":
+            nf = (m, n, p - 1)
+            out = np.zeros((r, m * n + n * (p - 1) + (p - 1) * m), np.int8)
+            rc = self.lib.or_meta_project(m, n, p, _p(c), r, _p(out), C.byref(rk))
+            out = out[: rk.value]
+        elif op == "extend":
+            nf = (m, n, p + 1)
+            out = np.zeros((r + m * n, m * n + n * (p + 1) + (p + 1) * m), np.int8)
+            rc = self.lib.or_meta_extend(m, n, p, _p(c), r, _p(out), C.byref(rk))
+        elif op in ("merge", "double"):
+            if op == "double":
+                fmt2, coeffs2 = fmt, coeffs
+            p2 = fmt2[2]
+            c2 = np.ascontiguousarray(coeffs2, dtype=np.int8)
+            nf = (m, n, p + p2)
+            out = np.zeros((r + c2.shape[0], m * n + n * (p + p2) + (p + p2) * m), np.int8)
+            rc = self.lib.or_meta_merge(m, n, p, p2, _p(c), r, _p(c2), c2.shape[0], _p(out))
+        elif op == "product":
+            m2, n2, p2 = fmt2
+            c2 = np.ascontiguousarray(coeffs2, dtype=np.int8)
+            M, N, P = m * m2, n * n2, p * p2
+            nf = (M, N, P)
+            out = np.zeros((r * c2.shape[0], M * N + N * P + P * M), np.int8)
+            rc = self.lib.or_meta_product(m, n, p, _p(c), r, m2, n2, p2, _p(c2), c2.shape[0], _p(out))
+        else:
+            raise ValueError(op)
+        if rc != 0:
+            raise ValueError(f"or_meta_{op}: {rc}")
+        return nf, out
 
     def matrix_rank(self, a):
         a = np.ascontiguousarray(a, dtype=np.int8)

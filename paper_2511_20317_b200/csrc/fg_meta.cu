@@ -1,0 +1,280 @@
+// fg_meta.cu -- host-side meta operators of PAPER:243-262 (section 3.3.2) on bit
+// planes: transpose, rotate, swap sizes, project, extend, merge, double, product.
+// They orchestrate between walks (north star: "pool-level meta operations stay in
+// plain host C orchestration outside the hot path"); readings R25-R30 in DESIGN.md.
+// Each operator is a fixed permutation / scatter of factor bits (an index map built
+// once per call) applied to the digit and sign words of every row; the product is
+// a Kronecker product of set bits.  Independent of oracle/meta.c.
+#include <cstring>
+#include <vector>
+#include "fg_internal.h"
+
+namespace {
+
+struct Sch {                         // one scheme as bit planes, format (m, n, p)
+    int m, n, p;
+    std::vector<uint64_t> d[3], s[3];    // per role, one word per row
+    int rank() const { return (int)d[0].size(); }
+    int len(int X) const { return X == 0 ? m * n : (X == 1 ? n * p : p * m); }
+};
+
+bool fmt_ok(int m, int n, int p)
+{
+    return m >= 1 && n >= 1 && p >= 1 && m * n <= 64 && n * p <= 64 && p * m <= 64;
+}
+
+int load(int m, int n, int p, int ring, const int8_t *in, int rank, Sch &o)
+{
+    if (!fmt_ok(m, n, p)) return FG_E_CAPACITY;
+    if (rank < 0 || (rank > 0 && !in)) return FG_E_ARG;
+    o.m = m; o.n = n; o.p = p;
+    const int w = m * n + n * p + p * m;
+    for (int X = 0; X < 3; ++X) { o.d[X].assign(rank, 0); o.s[X].assign(rank, 0); }
+    for (int l = 0; l < rank; ++l) {
+        int off = 0;
+        for (int X = 0; X < 3; ++X) {
+            for (int e = 0; e < o.len(X); ++e) {
+                const int v = in[(size_t)l * w + off + e];
+                if (v == 0) continue;
+                if (v == 1) o.d[X][l] |= 1ull << e;
+                else if (v == -1 && ring == FG_ZT) { o.d[X][l] |= 1ull << e; o.s[X][l] |= 1ull << e; }
+                else return FG_E_DOMAIN;
+            }
+            off += o.len(X);
+        }
+    }
+    return FG_OK;
+}
+
+void store(const Sch &a, int8_t *out)
+{
+    const int w = a.m * a.n + a.n * a.p + a.p * a.m;
+    for (int l = 0; l < a.rank(); ++l) {
+        int off = 0;
+        for (int X = 0; X < 3; ++X) {
+            for (int e = 0; e < a.len(X); ++e)
+                out[(size_t)l * w + off + e] = ((a.d[X][l] >> e) & 1) ? (((a.s[X][l] >> e) & 1) ? -1 : 1) : 0;
+            off += a.len(X);
+        }
+    }
+}
+
+// out bit map[e] <- in bit e (map[e] < 0: dropped)
+uint64_t scatter(uint64_t x, const std::vector<int> &map)
+{
+    uint64_t o = 0;
+    for (uint64_t t = x; t; t &= t - 1) {
+        const int e = __builtin_ctzll(t);
+        if (map[e] >= 0) o |= 1ull << map[e];
+    }
+    return o;
+}
+
+// role `dst` of b <- role `src` of a through the bit map
+void remap(const Sch &a, int src, Sch &b, int dst, const std::vector<int> &map)
+{
+    b.d[dst].resize(a.rank());
+    b.s[dst].resize(a.rank());
+    for (int l = 0; l < a.rank(); ++l) {
+        b.d[dst][l] = scatter(a.d[src][l], map);
+        b.s[dst][l] = scatter(a.s[src][l], map);
+    }
+}
+
+// transpose: C = AB <=> C^T = B^T A^T, (m,n,p) -> (p,n,m)
+Sch transpose(const Sch &a)
+{
+    const int m = a.m, n = a.n, p = a.p;
+    Sch b;
+    b.m = p; b.n = n; b.p = m;
+    std::vector<int> mu(m * n), mv(n * p), mw(p * m);
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) mu[i * n + j] = j * m + i;      // A_ij -> B'_ji (B' is n x m)
+    for (int j = 0; j < n; ++j)
+        for (int k = 0; k < p; ++k) mv[j * p + k] = k * n + j;      // B_jk -> A'_kj (A' is p x n)
+    for (int k = 0; k < p; ++k)
+        for (int i = 0; i < m; ++i) mw[k * m + i] = i * p + k;      // c_ik -> c'_ki, stored C'^T
+    remap(a, 1, b, 0, mv);
+    remap(a, 0, b, 1, mu);
+    remap(a, 2, b, 2, mw);
+    return b;
+}
+
+// cyclic symmetry: (u, v, w) -> (v, w, u), (m,n,p) -> (n,p,m), bit positions unchanged
+Sch rotate(const Sch &a)
+{
+    Sch b;
+    b.m = a.n; b.n = a.p; b.p = a.m;
+    b.d[0] = a.d[1]; b.s[0] = a.s[1];
+    b.d[1] = a.d[2]; b.s[1] = a.s[2];
+    b.d[2] = a.d[0]; b.s[2] = a.s[0];
+    return b;
+}
+
+// B, C column k of a (p columns) -> column off + k of P columns
+void columns(const Sch &a, int P, int off, Sch &b)
+{
+    const int m = a.m, n = a.n, p = a.p;
+    std::vector<int> mv(n * p), mw(p * m);
+    for (int j = 0; j < n; ++j)
+        for (int k = 0; k < p; ++k) mv[j * p + k] = (off + k) < P ? j * P + off + k : -1;
+    for (int k = 0; k < p; ++k)
+        for (int i = 0; i < m; ++i) mw[k * m + i] = (off + k) < P ? (off + k) * m + i : -1;
+    b.d[0] = a.d[0]; b.s[0] = a.s[0];
+    remap(a, 1, b, 1, mv);
+    remap(a, 2, b, 2, mw);
+}
+
+void append(Sch &a, const Sch &b)
+{
+    for (int X = 0; X < 3; ++X) {
+        a.d[X].insert(a.d[X].end(), b.d[X].begin(), b.d[X].end());
+        a.s[X].insert(a.s[X].end(), b.s[X].begin(), b.s[X].end());
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int fg_meta_transpose(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out)
+{
+    Sch a;
+    int rc = load(m, n, p, ring, in, rank, a);
+    if (rc != FG_OK) return rc;
+    if (!out) return FG_E_ARG;
+    store(transpose(a), out);
+    return FG_OK;
+}
+
+int fg_meta_rotate(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out)
+{
+    Sch a;
+    int rc = load(m, n, p, ring, in, rank, a);
+    if (rc != FG_OK) return rc;
+    if (!out) return FG_E_ARG;
+    store(rotate(a), out);
+    return FG_OK;
+}
+
+int fg_meta_swap_sizes(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out)
+{
+    Sch a;
+    int rc = load(m, n, p, ring, in, rank, a);
+    if (rc != FG_OK) return rc;
+    if (!out) return FG_E_ARG;
+    store(rotate(rotate(transpose(a))), out);   // (m,n,p) -> (p,n,m) -> (n,m,p) -> (m,p,n)
+    return FG_OK;
+}
+
+int fg_meta_project(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out, int *rank_out)
+{
+    Sch a;
+    if (p < 2) return FG_E_ARG;
+    int rc = load(m, n, p, ring, in, rank, a);
+    if (rc != FG_OK) return rc;
+    if (!out || !rank_out) return FG_E_ARG;
+    Sch b;
+    b.m = m; b.n = n; b.p = p - 1;
+    columns(a, p - 1, 0, b);                    // the last column of B and C is dropped
+    Sch c;
+    c.m = m; c.n = n; c.p = p - 1;
+    for (int l = 0; l < b.rank(); ++l) {        // terms with a zero factor vanish
+        if (!b.d[0][l] || !b.d[1][l] || !b.d[2][l]) continue;
+        for (int X = 0; X < 3; ++X) { c.d[X].push_back(b.d[X][l]); c.s[X].push_back(b.s[X][l]); }
+    }
+    store(c, out);
+    *rank_out = c.rank();
+    return FG_OK;
+}
+
+int fg_meta_extend(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out, int *rank_out)
+{
+    Sch a;
+    if (!fmt_ok(m, n, p + 1)) return FG_E_CAPACITY;
+    int rc = load(m, n, p, ring, in, rank, a);
+    if (rc != FG_OK) return rc;
+    if (!out || !rank_out) return FG_E_ARG;
+    Sch b;
+    b.m = m; b.n = n; b.p = p + 1;
+    columns(a, p + 1, 0, b);
+    Sch nv;                                       // naive (m,n,1) for the new column p
+    nv.m = m; nv.n = n; nv.p = p + 1;
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) {
+            nv.d[0].push_back(1ull << (i * n + j)); nv.s[0].push_back(0);
+            nv.d[1].push_back(1ull << (j * (p + 1) + p)); nv.s[1].push_back(0);
+            nv.d[2].push_back(1ull << (p * m + i)); nv.s[2].push_back(0);
+        }
+    append(b, nv);
+    store(b, out);
+    *rank_out = b.rank();
+    return FG_OK;
+}
+
+int fg_meta_merge(int m, int n, int p1, int p2, int ring, const int8_t *a_in, int ra, const int8_t *b_in, int rb,
+                  int8_t *out)
+{
+    if (!fmt_ok(m, n, p1 + p2)) return FG_E_CAPACITY;
+    Sch a, b;
+    int rc = load(m, n, p1, ring, a_in, ra, a);
+    if (rc == FG_OK) rc = load(m, n, p2, ring, b_in, rb, b);
+    if (rc != FG_OK) return rc;
+    if (!out) return FG_E_ARG;
+    const int P = p1 + p2;
+    Sch x, y;
+    x.m = y.m = m; x.n = y.n = n; x.p = y.p = P;
+    columns(a, P, 0, x);                          // C1 = A B1 in columns 0 .. p1-1
+    columns(b, P, p1, y);                         // C2 = A B2 in columns p1 .. P-1
+    append(x, y);
+    store(x, out);
+    return FG_OK;
+}
+
+int fg_meta_double(int m, int n, int p, int ring, const int8_t *in, int rank, int8_t *out)
+{
+    return fg_meta_merge(m, n, p, p, ring, in, rank, in, rank, out);
+}
+
+int fg_meta_product(int m1, int n1, int p1, const int8_t *a_in, int ra, int m2, int n2, int p2, const int8_t *b_in,
+                    int rb, int ring, int8_t *out)
+{
+    const int M = m1 * m2, N = n1 * n2, P = p1 * p2;
+    if (!fmt_ok(M, N, P)) return FG_E_CAPACITY;
+    Sch a, b;
+    int rc = load(m1, n1, p1, ring, a_in, ra, a);
+    if (rc == FG_OK) rc = load(m2, n2, p2, ring, b_in, rb, b);
+    if (rc != FG_OK) return rc;
+    if (!out) return FG_E_ARG;
+    // Kronecker index of (outer element e1 of a's factor, inner element e2 of b's)
+    auto kidx = [&](int X, int e1, int e2) {
+        int r1, c1, r2, c2, rows2, cols, cols1, cols2;
+        if (X == 0) { cols1 = n1; cols2 = n2; rows2 = m2; cols = N; }
+        else if (X == 1) { cols1 = p1; cols2 = p2; rows2 = n2; cols = P; }
+        else { cols1 = m1; cols2 = m2; rows2 = p2; cols = M; }
+        r1 = e1 / cols1; c1 = e1 % cols1; r2 = e2 / cols2; c2 = e2 % cols2;
+        return (r1 * rows2 + r2) * cols + (c1 * cols2 + c2);
+    };
+    Sch c;
+    c.m = M; c.n = N; c.p = P;
+    for (int l1 = 0; l1 < ra; ++l1)
+        for (int l2 = 0; l2 < rb; ++l2)
+            for (int X = 0; X < 3; ++X) {
+                uint64_t d = 0, s = 0;
+                for (uint64_t t1 = a.d[X][l1]; t1; t1 &= t1 - 1) {
+                    const int e1 = __builtin_ctzll(t1);
+                    for (uint64_t t2 = b.d[X][l2]; t2; t2 &= t2 - 1) {
+                        const int e2 = __builtin_ctzll(t2);
+                        const int E = kidx(X, e1, e2);
+                        d |= 1ull << E;
+                        if (ring == FG_ZT && (((a.s[X][l1] >> e1) ^ (b.s[X][l2] >> e2)) & 1)) s |= 1ull << E;
+                    }
+                }
+                c.d[X].push_back(d);
+                c.s[X].push_back(s);
+            }
+    store(c, out);
+    return FG_OK;
+}
+
+}  // extern "C"

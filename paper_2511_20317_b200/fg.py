@@ -69,6 +69,14 @@ _sig = {
     "fg_load_state": (_i32, [_vp, _vp]),
     "fg_stats": (_i32, [_vp, _vp]),
     "fg_kernel_name": (C.c_char_p, [_vp]),
+    "fg_meta_transpose": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
+    "fg_meta_rotate": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
+    "fg_meta_swap_sizes": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
+    "fg_meta_project": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "fg_meta_extend": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "fg_meta_merge": (_i32, [_i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp]),
+    "fg_meta_double": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
+    "fg_meta_product": (_i32, [_i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -147,6 +155,42 @@ def fg_record_merge(records: np.ndarray, count: int) -> np.ndarray:
     out = np.zeros(recs.size // count, np.uint8)
     _ck(_lib.fg_record_merge(_p(recs), count, _p(out)), "fg_record_merge")
     return out
+
+
+def fg_meta(op, fmt, coeffs, ring=FG_ZT, fmt2=None, coeffs2=None):
+    """Meta operator `op` of PAPER:243-262 on a scheme; returns ((m, n, p), coeffs)."""
+    m, n, p = fmt
+    c = np.ascontiguousarray(coeffs, dtype=np.int8)
+    r = c.shape[0]
+    rk = C.c_int(0)
+    w = lambda a, b, d: a * b + b * d + d * a          # noqa: E731
+    if op in ("transpose", "rotate", "swap_sizes", "double"):
+        nf = {"transpose": (p, n, m), "rotate": (n, p, m), "swap_sizes": (m, p, n),
+              "double": (m, n, 2 * p)}[op]
+        out = np.zeros((2 * r if op == "double" else r, w(*nf)), np.int8)
+        _ck(getattr(_lib, "fg_meta_" + op)(m, n, p, ring, _p(c), r, _p(out)), "fg_meta_" + op)
+        return nf, out
+    if op in ("project", "extend"):
+        nf = (m, n, p - 1) if op == "project" else (m, n, p + 1)
+        out = np.zeros((r + (m * n if op == "extend" else 0), w(*nf)), np.int8)
+        _ck(getattr(_lib, "fg_meta_" + op)(m, n, p, ring, _p(c), r, _p(out), C.byref(rk)),
+            "fg_meta_" + op)
+        return nf, out[: rk.value].copy()
+    c2 = np.ascontiguousarray(coeffs2, dtype=np.int8)
+    if op == "merge":
+        nf = (m, n, p + fmt2[2])
+        out = np.zeros((r + c2.shape[0], w(*nf)), np.int8)
+        _ck(_lib.fg_meta_merge(m, n, p, fmt2[2], ring, _p(c), r, _p(c2), c2.shape[0], _p(out)),
+            "fg_meta_merge")
+        return nf, out
+    if op == "product":
+        m2, n2, p2 = fmt2
+        nf = (m * m2, n * n2, p * p2)
+        out = np.zeros((r * c2.shape[0], w(*nf)), np.int8)
+        _ck(_lib.fg_meta_product(m, n, p, _p(c), r, m2, n2, p2, _p(c2), c2.shape[0], ring, _p(out)),
+            "fg_meta_product")
+        return nf, out
+    raise ValueError(op)
 
 
 class FlipGraph:

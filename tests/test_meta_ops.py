@@ -1,0 +1,108 @@
+"""Meta operators: libfg's host implementation (bit-plane index maps)
+against the oracle's (int8 definitions), byte-exact; every result verifies; ranks
+follow the stated formulas; paper / closed-form pins."""
+import numpy as np
+import pytest
+
+from golden_io import load_scheme
+from oracle import Oracle
+
+ZT, Z2 = 0, 1
+
+
+@pytest.fixture(scope="module")
+def fg():
+    from paper_2511_20317_b200.build import build_libfg
+    build_libfg()
+    from paper_2511_20317_b200 import fg as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+def _schemes(orc):
+    _, _, _, strassen = load_scheme("sec36_after.txt")
+    _, _, _, s223 = load_scheme("scheme_2x2x3_r11.txt")
+    w = orc.walker(3, 3, 3, ZT, 32, walker_id=2)
+    w.seed_naive()
+    w.walk(4000, 5)
+    out = [((2, 2, 2), ZT, strassen), ((2, 2, 3), ZT, s223), ((3, 3, 3), ZT, w.rows()),
+           ((2, 3, 4), ZT, orc.naive(2, 3, 4)), ((3, 2, 4), Z2, orc.naive(3, 2, 4))]
+    wz = orc.walker(2, 3, 3, Z2, 32, walker_id=4)
+    wz.seed_naive()
+    wz.walk(3000, 8)
+    out.append(((2, 3, 3), Z2, wz.rows()))
+    return out
+
+
+@pytest.mark.parametrize("op", ["transpose", "rotate", "swap_sizes", "project", "extend", "double"])
+def test_unary_ops_match_oracle_and_verify(fg, orc, op):
+    for fmt, ring, c in _schemes(orc):
+        if op == "project" and fmt[2] < 2:
+            continue
+        nf, got = fg.fg_meta(op, fmt, c, ring)
+        nf2, ref = orc.meta(op, fmt, c)
+        assert nf == nf2 and np.array_equal(got, ref), (op, fmt)
+        assert orc.verify(*nf, ring, got)[0] == 0, (op, fmt)
+        r = c.shape[0]
+        m, n, p = fmt
+        if op == "extend":
+            assert got.shape[0] == r + m * n
+        elif op == "double":
+            assert got.shape[0] == 2 * r
+        elif op == "project":
+            assert got.shape[0] <= r
+        else:
+            assert got.shape[0] == r
+
+
+def test_merge_strassen_with_naive_gives_the_printed_rank(fg, orc):
+    """merge((2,2,2:7), naive (2,2,1:4)) is a (2,2,3:11) scheme -- the rank of the
+    example printed at PAPER:130-175."""
+    _, _, _, strassen = load_scheme("sec36_after.txt")
+    nf, got = fg.fg_meta("merge", (2, 2, 2), strassen, ZT, (2, 2, 1), orc.naive(2, 2, 1))
+    assert nf == (2, 2, 3) and got.shape[0] == 11
+    assert orc.verify(2, 2, 3, ZT, got)[0] == 0
+    assert np.array_equal(got, orc.meta("merge", (2, 2, 2), strassen, (2, 2, 1), orc.naive(2, 2, 1))[1])
+
+
+def test_product_strassen_squared(fg, orc):
+    """Strassen x Strassen = (4,4,4:49), the Z_T rank of PAPER:699 (Table 5)."""
+    _, _, _, strassen = load_scheme("sec36_after.txt")
+    nf, got = fg.fg_meta("product", (2, 2, 2), strassen, ZT, (2, 2, 2), strassen)
+    assert nf == (4, 4, 4) and got.shape[0] == 49
+    assert orc.verify(4, 4, 4, ZT, got)[0] == 0
+    assert np.array_equal(got, orc.meta("product", (2, 2, 2), strassen, (2, 2, 2), strassen)[1])
+    # mixed formats and Z_2
+    for (f1, c1, f2, c2, ring) in [((2, 3, 1), orc.naive(2, 3, 1), (3, 1, 2), orc.naive(3, 1, 2), ZT),
+                                   ((2, 2, 2), strassen, (1, 2, 3), orc.naive(1, 2, 3), ZT),
+                                   ((2, 2, 2), np.abs(strassen), (2, 1, 2), orc.naive(2, 1, 2), Z2)]:
+        if ring == Z2 and orc.verify(*f1, Z2, c1)[0] != 0:
+            continue
+        nf, got = fg.fg_meta("product", f1, c1, ring, f2, c2)
+        assert np.array_equal(got, orc.meta("product", f1, c1, f2, c2)[1])
+        assert orc.verify(*nf, ring, got)[0] == 0
+
+
+def test_swap_is_an_involution_on_the_format_and_project_of_naive(fg, orc):
+    for fmt in [(2, 3, 4), (3, 3, 2)]:
+        c = orc.naive(*fmt)
+        nf, s1 = fg.fg_meta("swap_sizes", fmt, c)
+        nf2, s2 = fg.fg_meta("swap_sizes", nf, s1)
+        assert nf2 == fmt and orc.verify(*fmt, ZT, s2)[0] == 0
+        nf, pr = fg.fg_meta("project", fmt, c)
+        assert pr.shape[0] == fmt[0] * fmt[1] * (fmt[2] - 1)          # naive (m,n,p-1)
+        assert orc.additions(*nf, pr) == nf[0] * nf[2] * (nf[1] - 1)
+
+
+def test_capacity_and_domain_errors(fg, orc):
+    c = orc.naive(4, 4, 4)
+    with pytest.raises(fg.FgError):
+        fg.fg_meta("product", (4, 4, 4), c, ZT, (3, 3, 3), orc.naive(3, 3, 3))   # 12x12 > 64 elements
+    bad = orc.naive(2, 2, 2)
+    bad[0, 0] = 2
+    with pytest.raises(fg.FgError):
+        fg.fg_meta("transpose", (2, 2, 2), bad)
