@@ -217,6 +217,19 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
             change_factor(t, 1, nr.v);
             change_factor(t, 2, nr.w);
         };
+        // after a flip only factor X of row t can change class (normalisation negates
+        // the changed factor and w, whose class is sign-free); other factors of t may
+        // change sign only: plain stores
+        auto put_flip_row = [&](int t, int X, const Row<P> &nr) {
+            change_factor(t, X, get(nr, X));
+            if (lane == 0) {
+                const int pt = ph(t);
+                if (X != 0) sf[0 * PLANE + pt] = nr.u;
+                if (X != 1) sf[1 * PLANE + pt] = nr.v;
+                if (X != 2) sf[2 * PLANE + pt] = nr.w;
+            }
+            __syncwarp();
+        };
         auto append_row = [&](const Row<P> &nr) {
             const int t = r;
             __syncwarp();
@@ -527,8 +540,11 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     }
                     ex -= cb;
                     const int M = __ffs(__ballot_sync(FULL, ex <= q2 && q2 < ex + cb)) - 1;
-                    uint32_t bm = bits, tt = q2 - ex;
-                    for (int z = 0; z < NS && tt; ++z) { if (bm) bm &= bm - 1; --tt; }
+                    uint32_t bm = bits;
+                    const uint32_t tt = q2 - ex;     // garbage (large) off lane M: bounded below
+                    bm = tt > 0 ? (bm & (bm - 1u)) : bm;
+                    bm = tt > 1 ? (bm & (bm - 1u)) : bm;
+                    for (uint32_t z = 2; z < tt && z < NS; ++z) bm &= bm - 1u;
                     const int jsl = __shfl_sync(FULL, __ffs(bm) - 1, M);
                     const int j = M * NS + jsl;
                     const int al = d ? j : i, be = d ? i : j;
@@ -548,8 +564,8 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     set(nb, Z, nz, true);
                     normalize<P>(na);
                     normalize<P>(nb);
-                    put_row(al, na);
-                    put_row(be, nb);
+                    put_flip_row(al, Y, na);
+                    put_flip_row(be, Z, nb);
                     if (cmode) nnz_cur += popr(na) + popr(nb) - popr(ra) - popr(rb);
                     alpha = al;
                     beta = be;
