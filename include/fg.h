@@ -212,6 +212,17 @@ int fg_meta_double(int m, int n, int p, int ring, const int8_t *in, int rank, in
 int fg_meta_product(int m1, int n1, int p1, const int8_t *a, int ra, int m2, int n2, int p2, const int8_t *b,
                     int rb, int ring, int8_t *out);
 
+/* Type invariant: counts[(ru*65 + rv)*65 + rw] = number of terms whose
+   U, V, W factor matrices (m x n, n x p, p x m) have ranks (ru, rv, rw) over Q;
+   rank_sums = the exponents of the rank-sum polynomial.  The
+   symmetrised polynomial is the S_3 orbit sum of the type counts.
+   counts must hold 65^3 ints.  Host only. */
+int fg_type_invariant(int m, int n, int p, int ring, const int8_t *coeffs, int rank, int32_t *counts,
+                      int32_t rank_sums[3]);
+/* Canonical 64-bit key of a scheme up to row order and per-row sign normalisation
+   (PAPER:429): for pool de-duplication.  Host only. */
+int fg_scheme_key(int m, int n, int p, int ring, const int8_t *coeffs, int rank, uint64_t *key);
+
 /* Which kernel variant fg_walk uses for this ctx ("warp32_zt_u32k", ...). */
 const char *fg_kernel_name(const fg_ctx *ctx);
 

@@ -5,6 +5,8 @@
 // Each operator is a fixed permutation / scatter of factor bits (an index map built
 // once per call) applied to the digit and sign words of every row; the product is
 // a Kronecker product of set bits.  Independent of oracle/meta.c.
+#include <algorithm>
+#include <array>
 #include <cstring>
 #include <vector>
 #include "fg_internal.h"
@@ -274,6 +276,88 @@ int fg_meta_product(int m1, int n1, int p1, const int8_t *a_in, int ra, int m2, 
                 c.s[X].push_back(s);
             }
     store(c, out);
+    return FG_OK;
+}
+
+// ---- isotropy invariants and a canonical key for pool dedup ----
+// Rank over Q of a factor matrix, computed over GF(2^31 - 1): every minor of a
+// ternary matrix with rows*cols <= 64 has order <= 8, so |minor| <= 8^4 (Hadamard)
+// < 2^31 - 1 and the modular rank equals the rational one.
+static int rank_mod_p(const int8_t *a, int rows, int cols)
+{
+    const int64_t P = 2147483647;
+    int64_t M[64][64];
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) M[r][c] = ((int64_t)a[r * cols + c] % P + P) % P;
+    auto inv = [&](int64_t x) {           // Fermat inverse
+        int64_t res = 1, b = x, e = P - 2;
+        while (e) { if (e & 1) res = res * b % P; b = b * b % P; e >>= 1; }
+        return res;
+    };
+    int rank = 0;
+    for (int c = 0; c < cols && rank < rows; ++c) {
+        int piv = -1;
+        for (int r = rank; r < rows; ++r) if (M[r][c]) { piv = r; break; }
+        if (piv < 0) continue;
+        for (int k = 0; k < cols; ++k) std::swap(M[piv][k], M[rank][k]);
+        const int64_t iv = inv(M[rank][c]);
+        for (int r = rank + 1; r < rows; ++r) {
+            if (!M[r][c]) continue;
+            const int64_t f = M[r][c] * iv % P;
+            for (int k = c; k < cols; ++k) M[r][k] = ((M[r][k] - f * M[rank][k]) % P + P) % P;
+        }
+        rank++;
+    }
+    return rank;
+}
+
+int fg_type_invariant(int m, int n, int p, int ring, const int8_t *coeffs, int rank, int32_t *counts,
+                      int32_t rank_sums[3])
+{
+    Sch a;
+    int rc = load(m, n, p, ring, coeffs, rank, a);
+    if (rc != FG_OK) return rc;
+    if (!counts || !rank_sums) return FG_E_ARG;
+    memset(counts, 0, sizeof(int32_t) * 65 * 65 * 65);
+    rank_sums[0] = rank_sums[1] = rank_sums[2] = 0;
+    const int dims[3][2] = {{m, n}, {n, p}, {p, m}};    // U: m x n, V: n x p, W: p x m (C^T)
+    int8_t buf[64];
+    for (int l = 0; l < rank; ++l) {
+        int rk[3];
+        for (int X = 0; X < 3; ++X) {
+            const int len = dims[X][0] * dims[X][1];
+            for (int e = 0; e < len; ++e)
+                buf[e] = ((a.d[X][l] >> e) & 1) ? (((a.s[X][l] >> e) & 1) ? -1 : 1) : 0;
+            rk[X] = rank_mod_p(buf, dims[X][0], dims[X][1]);
+            rank_sums[X] += rk[X];
+        }
+        counts[(rk[0] * 65 + rk[1]) * 65 + rk[2]] += 1;
+    }
+    return FG_OK;
+}
+
+// canonical key: rows sign-normalised (Z_T), sorted, hashed (FNV-1a over the words);
+// equal schemes up to row order and the sign rescaling of PAPER:429 share a key
+int fg_scheme_key(int m, int n, int p, int ring, const int8_t *coeffs, int rank, uint64_t *key)
+{
+    Sch a;
+    int rc = load(m, n, p, ring, coeffs, rank, a);
+    if (rc != FG_OK) return rc;
+    if (!key) return FG_E_ARG;
+    std::vector<std::array<uint64_t, 6>> rows(rank);
+    for (int l = 0; l < rank; ++l) {
+        uint64_t ud = a.d[0][l], us = a.s[0][l], vd = a.d[1][l], vs = a.s[1][l], wd = a.d[2][l], ws = a.s[2][l];
+        if (ring == FG_ZT) {
+            if (us & (ud & (0 - ud))) { us ^= ud; ws ^= wd; }
+            if (vs & (vd & (0 - vd))) { vs ^= vd; ws ^= wd; }
+        }
+        rows[l] = {ud, us, vd, vs, wd, ws};
+    }
+    std::sort(rows.begin(), rows.end());
+    uint64_t h = 0xcbf29ce484222325ULL ^ ((uint64_t)m << 48 | (uint64_t)n << 32 | (uint64_t)p << 16 | (uint64_t)ring);
+    for (const auto &r : rows)
+        for (uint64_t x : r) { h ^= x; h *= 0x100000001b3ULL; }
+    *key = h;
     return FG_OK;
 }
 

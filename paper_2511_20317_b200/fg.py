@@ -77,6 +77,8 @@ _sig = {
     "fg_meta_merge": (_i32, [_i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp]),
     "fg_meta_double": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
     "fg_meta_product": (_i32, [_i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
+    "fg_type_invariant": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "fg_scheme_key": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -155,6 +157,28 @@ def fg_record_merge(records: np.ndarray, count: int) -> np.ndarray:
     out = np.zeros(recs.size // count, np.uint8)
     _ck(_lib.fg_record_merge(_p(recs), count, _p(out)), "fg_record_merge")
     return out
+
+
+def fg_type_invariant(m, n, p, ring, coeffs):
+    """({(ru, rv, rw): count}, (sum ru, sum rv, sum rw)) -- PAPER:515-524."""
+    c = np.ascontiguousarray(coeffs, dtype=np.int8)
+    counts = np.zeros(65 ** 3, np.int32)
+    sums = np.zeros(3, np.int32)
+    _ck(_lib.fg_type_invariant(m, n, p, ring, _p(c), c.shape[0], _p(counts), _p(sums)),
+        "fg_type_invariant")
+    out = {}
+    for idx in np.nonzero(counts)[0]:
+        ru, rest = divmod(int(idx), 65 * 65)
+        rv, rw = divmod(rest, 65)
+        out[(ru, rv, rw)] = int(counts[idx])
+    return out, tuple(int(x) for x in sums)
+
+
+def fg_scheme_key(m, n, p, ring, coeffs) -> int:
+    c = np.ascontiguousarray(coeffs, dtype=np.int8)
+    k = C.c_uint64()
+    _ck(_lib.fg_scheme_key(m, n, p, ring, _p(c), c.shape[0], C.byref(k)), "fg_scheme_key")
+    return k.value
 
 
 def fg_meta(op, fmt, coeffs, ring=FG_ZT, fmt2=None, coeffs2=None):

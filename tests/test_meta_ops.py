@@ -106,3 +106,28 @@ def test_capacity_and_domain_errors(fg, orc):
     bad[0, 0] = 2
     with pytest.raises(fg.FgError):
         fg.fg_meta("transpose", (2, 2, 2), bad)
+
+
+def test_invariants_match_oracle_and_paper(fg, orc):
+    """PAPER:515-524 on the rank-7 example: type X^2Y^2Z^2 + 6XYZ, rank sums (8,8,8);
+    libfg (rank over GF(2^31-1)) equals the oracle (Bareiss over Q) everywhere."""
+    m, n, p, s = load_scheme("sec36_after.txt")
+    t, sums = fg.fg_type_invariant(m, n, p, ZT, s)
+    assert t == {(2, 2, 2): 1, (1, 1, 1): 6} and sums == (8, 8, 8)
+    for fmt, ring, c in _schemes(orc):
+        t, sums = fg.fg_type_invariant(*fmt, ring, c)
+        if ring == ZT:
+            assert t == orc.type_invariant(*fmt, c)
+        assert sum(t.values()) == c.shape[0]
+    nf, sq = fg.fg_meta("product", (2, 2, 2), s, ZT, (2, 2, 2), s)
+    assert fg.fg_type_invariant(*nf, ZT, sq)[0] == orc.type_invariant(*nf, sq)
+
+
+def test_scheme_key_is_invariant_under_row_order_and_sign(fg, orc):
+    m, n, p, before = load_scheme("sec36_before.txt")
+    _, _, _, after = load_scheme("sec36_after.txt")
+    k = fg.fg_scheme_key(m, n, p, ZT, after)
+    assert fg.fg_scheme_key(m, n, p, ZT, before) == k          # PAPER:431-497: same scheme
+    rng = np.random.default_rng(0)
+    assert fg.fg_scheme_key(m, n, p, ZT, after[rng.permutation(7)]) == k
+    assert fg.fg_scheme_key(m, n, p, ZT, orc.naive(2, 2, 2)) != k
