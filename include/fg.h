@@ -212,6 +212,21 @@ int fg_meta_double(int m, int n, int p, int ring, const int8_t *in, int rank, in
 int fg_meta_product(int m1, int n1, int p1, const int8_t *a, int ra, int m2, int n2, int p2, const int8_t *b,
                     int rb, int ring, int8_t *out);
 
+/* Alg. 2 Resize of one scheme, reading R31 in DESIGN.md; host only.
+   Decisions come from Philox blocks 0x100 / 0x101 of counter (round lo, round hi,
+   walker id, block) under key `seed`: swap sizes with probability 1/2; try to merge
+   with a best scheme picked uniformly (same m and n); if not merged, with
+   probability thr_resize/2^32: project 5% / product with a best scheme 50% / double
+   30% / extend 15%.  A result outside R1, max(m,n,p) <= 16
+   or rank <= r_cap is not applied.  (m,n,p), rank and coeffs are updated in place;
+   coeffs must hold r_cap rows of the widest format (3*64 int8).  bests: nbest
+   schemes, formats bfmt[3k..3k+2], ranks brank[k], rows bcoeffs[k].  op_out (may
+   be NULL): bit 0 = swapped; bits 1..3 = 1 merge, 2 project, 3 product, 4 double,
+   5 extend, 0 none.  Outputs are not sign-normalised. */
+int fg_resize(int *m, int *n, int *p, int ring, int8_t *coeffs, int *rank, int r_cap, int nbest,
+              const int32_t *bfmt, const int32_t *brank, const int8_t *const *bcoeffs, uint32_t thr_resize,
+              uint64_t seed, uint64_t round, uint64_t walker_id, int *op_out);
+
 /* Type invariant: counts[(ru*65 + rv)*65 + rw] = number of terms whose
    U, V, W factor matrices (m x n, n x p, p x m) have ranks (ru, rv, rw) over Q;
    rank_sums = the exponents of the rank-sum polynomial.  The

@@ -183,3 +183,98 @@ int or_meta_product(int m1, int n1, int p1, const int8_t *a, int ra, int m2, int
         }
     return 0;
 }
+
+/* ---------- Alg. 2 Resize, reading R31 ----------
+   Decisions from Philox blocks 0x100 and 0x101 of counter (round lo, round hi,
+   walker id, block) under key `seed`: x0 < 2^31 -> swap sizes; x1 picks the best
+   scheme to try to merge with (same m, n); if not merged and x2 < thr_resize, x3
+   picks project (< 0.05) / product with the best picked by y0 (< 0.55) / double
+   (< 0.85) / extend.  A result violating R1, max(m,n,p) <= 16
+    or r_cap leaves the scheme unchanged.  op_out: bit 0 swapped,
+   bits 1.. = 1 merge, 2 project, 3 product, 4 double, 5 extend (0 none). */
+static int fits(int m, int n, int p, int rank, int r_cap)
+{
+    return fmt_ok(m, n, p) && m <= 16 && n <= 16 && p <= 16 && rank >= 1 && rank <= r_cap;
+}
+
+static uint32_t uni(uint32_t x, uint32_t n) { return (uint32_t)(((uint64_t)x * n) >> 32); }
+
+int or_resize(int *m, int *n, int *p, int8_t *coeffs, int *rank, int r_cap, int nbest, const int32_t *bfmt,
+              const int32_t *brank, const int8_t *const *bcoeffs, uint32_t thr_resize, uint64_t seed,
+              uint64_t round, uint64_t walker_id, int *op_out)
+{
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t c0[4] = {(uint32_t)round, (uint32_t)(round >> 32), (uint32_t)walker_id, 0x100};
+    uint32_t c1[4] = {(uint32_t)round, (uint32_t)(round >> 32), (uint32_t)walker_id, 0x101};
+    uint32_t x[4], y[4];
+    int M = *m, N = *n, P = *p, r = *rank, op = 0, merged = 0;
+    int8_t *tmp = (int8_t *)malloc((size_t)(r_cap + 1) * 3 * OR_MAXLEN + 64);
+    or_philox4x32_10(c0, key, x);
+    or_philox4x32_10(c1, key, y);
+    if (x[0] < 0x80000000u) {
+        or_meta_swap_sizes(M, N, P, coeffs, r, tmp);
+        memcpy(coeffs, tmp, (size_t)r * (M * N + N * P + P * M));
+        { int t = N; N = P; P = t; }
+        op |= 1;
+    }
+    if (nbest > 0) {
+        int b = (int)uni(x[1], (uint32_t)nbest);
+        if (bfmt[3 * b] == M && bfmt[3 * b + 1] == N && fits(M, N, P + bfmt[3 * b + 2], r + brank[b], r_cap)) {
+            or_meta_merge(M, N, P, bfmt[3 * b + 2], coeffs, r, bcoeffs[b], brank[b], tmp);
+            P += bfmt[3 * b + 2];
+            r += brank[b];
+            memcpy(coeffs, tmp, (size_t)r * (M * N + N * P + P * M));
+            merged = 1;
+            op |= 1 << 1;
+        }
+    }
+    if (!merged && x[2] < thr_resize) {
+        uint32_t q = x[3];
+        if (q < 214748364u) {                        /* 5% project */
+            int nr = 0;
+            if (P >= 2 && fits(M, N, P - 1, 1, r_cap)) {
+                or_meta_project(M, N, P, coeffs, r, tmp, &nr);
+                if (nr >= 1) {
+                    P -= 1;
+                    r = nr;
+                    memcpy(coeffs, tmp, (size_t)r * (M * N + N * P + P * M));
+                    op |= 2 << 1;
+                }
+            }
+        } else if (q < 2362232012u) {               /* 50% product with a best scheme */
+            if (nbest > 0) {
+                int b = (int)uni(y[0], (uint32_t)nbest);
+                int m2 = bfmt[3 * b], n2 = bfmt[3 * b + 1], p2 = bfmt[3 * b + 2];
+                if (fits(M * m2, N * n2, P * p2, r * brank[b], r_cap)) {
+                    int8_t *big = (int8_t *)malloc((size_t)r * brank[b] * 3 * OR_MAXLEN + 64);
+                    or_meta_product(M, N, P, coeffs, r, m2, n2, p2, bcoeffs[b], brank[b], big);
+                    M *= m2; N *= n2; P *= p2; r *= brank[b];
+                    memcpy(coeffs, big, (size_t)r * (M * N + N * P + P * M));
+                    free(big);
+                    op |= 3 << 1;
+                }
+            }
+        } else if (q < 3650722201u) {               /* 30% double */
+            if (fits(M, N, 2 * P, 2 * r, r_cap)) {
+                or_meta_merge(M, N, P, P, coeffs, r, coeffs, r, tmp);
+                P *= 2;
+                r *= 2;
+                memcpy(coeffs, tmp, (size_t)r * (M * N + N * P + P * M));
+                op |= 4 << 1;
+            }
+        } else {                                     /* 15% extend */
+            int nr = 0;
+            if (fits(M, N, P + 1, r + M * N, r_cap)) {
+                or_meta_extend(M, N, P, coeffs, r, tmp, &nr);
+                P += 1;
+                r = nr;
+                memcpy(coeffs, tmp, (size_t)r * (M * N + N * P + P * M));
+                op |= 5 << 1;
+            }
+        }
+    }
+    free(tmp);
+    *m = M; *n = N; *p = P; *rank = r;
+    if (op_out) *op_out = op;
+    return 0;
+}

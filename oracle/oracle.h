@@ -122,6 +122,10 @@ int or_meta_merge(int m, int n, int p1, int p2, const int8_t *a, int ra, const i
 int or_meta_product(int m1, int n1, int p1, const int8_t *a, int ra, int m2, int n2, int p2, const int8_t *b,
                     int rb, int8_t *out);
 
+int or_resize(int *m, int *n, int *p, int8_t *coeffs, int *rank, int r_cap, int nbest, const int32_t *bfmt,
+              const int32_t *brank, const int8_t *const *bcoeffs, uint32_t thr_resize, uint64_t seed,
+              uint64_t round, uint64_t walker_id, int *op_out);                 /* Alg. 2, R31 */
+
 /* many walkers in one flat call (bench cpu baseline / tests): walker k has global
    id id_base+k, all seeded naive (or from coeffs if rank>0).  Output per walker:
    r, best_r, digest, cnt[OR_NCNT], and optionally rows/best (R*(mn+np+pm) int8). */

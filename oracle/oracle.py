@@ -94,6 +94,7 @@ class Oracle:
         lib.or_meta_extend.argtypes = [i32, i32, i32, vp, i32, vp, vp]
         lib.or_meta_merge.argtypes = [i32, i32, i32, i32, vp, i32, vp, i32, vp]
         lib.or_meta_product.argtypes = [i32, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]
+        lib.or_resize.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, C.c_uint32, u64, u64, u64, vp]
         lib.or_run_walkers.argtypes = [i32, i32, i32, i32, i32, i64, u64, vp, vp, i32, u64, u64,
                                        vp, i32, vp, vp, vp, vp, vp, vp]
 
@@ -191,6 +192,25 @@ class Oracle:
         if rc != 0:
             raise ValueError(f"or_meta_{op}: {rc}")
         return nf, out
+
+    def resize(self, fmt, coeffs, bests, r_cap, seed, rnd, walker_id, thr_resize=1 << 31):
+        m_, n_, p_ = (C.c_int(x) for x in fmt)
+        c = np.ascontiguousarray(coeffs, dtype=np.int8)
+        buf = np.zeros(r_cap * 192 + 64, np.int8)
+        buf[: c.size] = c.reshape(-1)
+        rk = C.c_int(c.shape[0])
+        nb = len(bests)
+        bfmt = np.array([b[0] for b in bests], dtype=np.int32).reshape(-1) if nb else np.zeros(3, np.int32)
+        brank = np.array([len(b[1]) for b in bests], dtype=np.int32) if nb else np.zeros(1, np.int32)
+        keep = [np.ascontiguousarray(b[1], dtype=np.int8) for b in bests]
+        ptrs = (C.c_void_p * max(nb, 1))(*[k.ctypes.data for k in keep])
+        op = C.c_int(0)
+        self.lib.or_resize(C.byref(m_), C.byref(n_), C.byref(p_), _p(buf), C.byref(rk), r_cap, nb,
+                           _p(bfmt), _p(brank), C.cast(ptrs, C.c_void_p), thr_resize, seed, rnd,
+                           walker_id, C.byref(op))
+        nf = (m_.value, n_.value, p_.value)
+        w = nf[0] * nf[1] + nf[1] * nf[2] + nf[2] * nf[0]
+        return nf, buf[: rk.value * w].reshape(rk.value, w).copy(), op.value
 
     def matrix_rank(self, a):
         a = np.ascontiguousarray(a, dtype=np.int8)

@@ -279,6 +279,125 @@ int fg_meta_product(int m1, int n1, int p1, const int8_t *a_in, int ra, int m2, 
     return FG_OK;
 }
 
+// ---- Alg. 2 Resize, reading R31 ----
+static void philox_host(uint32_t c[4], uint32_t k0, uint32_t k1, uint32_t o[4])
+{
+    uint32_t x0 = c[0], x1 = c[1], x2 = c[2], x3 = c[3];
+    for (int i = 0; i < 10; ++i) {
+        if (i) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        const uint64_t a = (uint64_t)0xD2511F53u * x0, b = (uint64_t)0xCD9E8D57u * x2;
+        const uint32_t n0 = (uint32_t)(b >> 32) ^ x1 ^ k0, n2 = (uint32_t)(a >> 32) ^ x3 ^ k1;
+        x0 = n0; x1 = (uint32_t)b; x2 = n2; x3 = (uint32_t)a;
+    }
+    o[0] = x0; o[1] = x1; o[2] = x2; o[3] = x3;
+}
+
+static bool envelope(int m, int n, int p, int rank, int r_cap)
+{
+    return fmt_ok(m, n, p) && m <= 16 && n <= 16 && p <= 16 && rank >= 1 && rank <= r_cap;
+}
+
+int fg_resize(int *m, int *n, int *p, int ring, int8_t *coeffs, int *rank, int r_cap, int nbest,
+              const int32_t *bfmt, const int32_t *brank, const int8_t *const *bcoeffs, uint32_t thr_resize,
+              uint64_t seed, uint64_t round, uint64_t walker_id, int *op_out)
+{
+    if (!m || !n || !p || !coeffs || !rank || r_cap < 1 || nbest < 0 || (nbest > 0 && (!bfmt || !brank || !bcoeffs)))
+        return FG_E_ARG;
+    Sch a;
+    int rc = load(*m, *n, *p, ring, coeffs, *rank, a);
+    if (rc != FG_OK) return rc;
+    uint32_t c0[4] = {(uint32_t)round, (uint32_t)(round >> 32), (uint32_t)walker_id, 0x100u};
+    uint32_t c1[4] = {(uint32_t)round, (uint32_t)(round >> 32), (uint32_t)walker_id, 0x101u};
+    uint32_t x[4], y[4];
+    philox_host(c0, (uint32_t)seed, (uint32_t)(seed >> 32), x);
+    philox_host(c1, (uint32_t)seed, (uint32_t)(seed >> 32), y);
+    auto pick = [&](uint32_t w) { return (int)(((uint64_t)w * (uint32_t)nbest) >> 32); };
+    int op = 0;
+    if (x[0] < 0x80000000u) { a = rotate(rotate(transpose(a))); op |= 1; }       // swap sizes
+    bool merged = false;
+    if (nbest > 0) {
+        const int b = pick(x[1]);
+        if (bfmt[3 * b] == a.m && bfmt[3 * b + 1] == a.n &&
+            envelope(a.m, a.n, a.p + bfmt[3 * b + 2], a.rank() + brank[b], r_cap)) {
+            Sch bb;
+            rc = load(bfmt[3 * b], bfmt[3 * b + 1], bfmt[3 * b + 2], ring, bcoeffs[b], brank[b], bb);
+            if (rc != FG_OK) return rc;
+            const int P = a.p + bb.p;
+            Sch x1, y1;
+            x1.m = y1.m = a.m; x1.n = y1.n = a.n; x1.p = y1.p = P;
+            columns(a, P, 0, x1);
+            columns(bb, P, a.p, y1);
+            append(x1, y1);
+            a = x1;
+            merged = true;
+            op |= 1 << 1;
+        }
+    }
+    if (!merged && x[2] < thr_resize) {
+        const uint32_t q = x[3];
+        if (q < 214748364u) {                                   // 5% project
+            if (a.p >= 2 && envelope(a.m, a.n, a.p - 1, 1, r_cap)) {
+                Sch b;
+                b.m = a.m; b.n = a.n; b.p = a.p - 1;
+                columns(a, a.p - 1, 0, b);
+                Sch c;
+                c.m = b.m; c.n = b.n; c.p = b.p;
+                for (int l = 0; l < b.rank(); ++l) {
+                    if (!b.d[0][l] || !b.d[1][l] || !b.d[2][l]) continue;
+                    for (int X = 0; X < 3; ++X) { c.d[X].push_back(b.d[X][l]); c.s[X].push_back(b.s[X][l]); }
+                }
+                if (c.rank() >= 1) { a = c; op |= 2 << 1; }
+            }
+        } else if (q < 2362232012u) {                           // 50% product with a best scheme
+            if (nbest > 0) {
+                const int b = pick(y[0]);
+                const int m2 = bfmt[3 * b], n2 = bfmt[3 * b + 1], p2 = bfmt[3 * b + 2];
+                if (envelope(a.m * m2, a.n * n2, a.p * p2, a.rank() * brank[b], r_cap)) {
+                    std::vector<int8_t> cur((size_t)a.rank() * (a.m * a.n + a.n * a.p + a.p * a.m));
+                    store(a, cur.data());
+                    const int M = a.m * m2, N = a.n * n2, P = a.p * p2, R = a.rank() * brank[b];
+                    std::vector<int8_t> outv((size_t)R * (M * N + N * P + P * M));
+                    rc = fg_meta_product(a.m, a.n, a.p, cur.data(), a.rank(), m2, n2, p2, bcoeffs[b], brank[b], ring,
+                                         outv.data());
+                    if (rc != FG_OK) return rc;
+                    rc = load(M, N, P, ring, outv.data(), R, a);
+                    if (rc != FG_OK) return rc;
+                    op |= 3 << 1;
+                }
+            }
+        } else if (q < 3650722201u) {                           // 30% double
+            if (envelope(a.m, a.n, 2 * a.p, 2 * a.rank(), r_cap)) {
+                const int P = 2 * a.p;
+                Sch x1, y1;
+                x1.m = y1.m = a.m; x1.n = y1.n = a.n; x1.p = y1.p = P;
+                columns(a, P, 0, x1);
+                columns(a, P, a.p, y1);
+                append(x1, y1);
+                a = x1;
+                op |= 4 << 1;
+            }
+        } else {                                                // 15% extend
+            if (envelope(a.m, a.n, a.p + 1, a.rank() + a.m * a.n, r_cap)) {
+                Sch b;
+                b.m = a.m; b.n = a.n; b.p = a.p + 1;
+                columns(a, a.p + 1, 0, b);
+                for (int i = 0; i < a.m; ++i)
+                    for (int j = 0; j < a.n; ++j) {
+                        b.d[0].push_back(1ull << (i * a.n + j)); b.s[0].push_back(0);
+                        b.d[1].push_back(1ull << (j * (a.p + 1) + a.p)); b.s[1].push_back(0);
+                        b.d[2].push_back(1ull << (a.p * a.m + i)); b.s[2].push_back(0);
+                    }
+                a = b;
+                op |= 5 << 1;
+            }
+        }
+    }
+    store(a, coeffs);
+    *m = a.m; *n = a.n; *p = a.p; *rank = a.rank();
+    if (op_out) *op_out = op;
+    return FG_OK;
+}
+
 // ---- isotropy invariants and a canonical key for pool dedup ----
 // Rank over Q of a factor matrix, computed over GF(2^31 - 1): every minor of a
 // ternary matrix with rows*cols <= 64 has order <= 8, so |minor| <= 8^4 (Hadamard)

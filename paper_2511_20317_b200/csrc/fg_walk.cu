@@ -30,6 +30,9 @@ using namespace fgd;
 #define W32_THREADS 128
 #define W32_WARPS (W32_THREADS / 32)
 #define PXS 9                        // words per step in the Philox table (8 + 1 pad)
+#ifndef W32_MINB
+#define W32_MINB 8
+#endif
 
 namespace {
 
@@ -46,7 +49,7 @@ __device__ __forceinline__ int nth_bit(uint32_t x, uint32_t t)
 }
 
 template <class P, bool CM>
-__global__ void __launch_bounds__(W32_THREADS, 8) walk_w32(WalkArgs a)
+__global__ void __launch_bounds__(W32_THREADS, W32_MINB) walk_w32(WalkArgs a)
 {
     typedef typename P::F F;
     __shared__ uint32_t px_all[W32_WARPS][32 * PXS];

@@ -77,6 +77,8 @@ _sig = {
     "fg_meta_merge": (_i32, [_i32, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _i32, _vp]),
     "fg_meta_double": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
     "fg_meta_product": (_i32, [_i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
+    "fg_resize": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _vp, C.c_uint32, _u64,
+                          _u64, _u64, _vp]),
     "fg_type_invariant": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "fg_scheme_key": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
 }
@@ -157,6 +159,28 @@ def fg_record_merge(records: np.ndarray, count: int) -> np.ndarray:
     out = np.zeros(recs.size // count, np.uint8)
     _ck(_lib.fg_record_merge(_p(recs), count, _p(out)), "fg_record_merge")
     return out
+
+
+def fg_resize(fmt, coeffs, bests, r_cap, seed, rnd, walker_id, ring=FG_ZT, thr_resize=1 << 31):
+    """Alg. 2 on one scheme; bests: list of ((m,n,p), coeffs).
+    Returns ((m, n, p), coeffs, op)."""
+    m_, n_, p_ = (C.c_int(x) for x in fmt)
+    c = np.ascontiguousarray(coeffs, dtype=np.int8)
+    buf = np.zeros(r_cap * 192, np.int8)
+    buf[: c.size] = c.reshape(-1)
+    rk = C.c_int(c.shape[0])
+    nb = len(bests)
+    bfmt = np.array([b[0] for b in bests], dtype=np.int32).reshape(-1) if nb else np.zeros(3, np.int32)
+    brank = np.array([len(b[1]) for b in bests], dtype=np.int32) if nb else np.zeros(1, np.int32)
+    keep = [np.ascontiguousarray(b[1], dtype=np.int8) for b in bests]
+    ptrs = (C.c_void_p * max(nb, 1))(*[k.ctypes.data for k in keep])
+    op = C.c_int(0)
+    _ck(_lib.fg_resize(C.byref(m_), C.byref(n_), C.byref(p_), ring, _p(buf), C.byref(rk), r_cap, nb,
+                       _p(bfmt), _p(brank), C.cast(ptrs, C.c_void_p), thr_resize, seed, rnd, walker_id,
+                       C.byref(op)), "fg_resize")
+    nf = (m_.value, n_.value, p_.value)
+    w = nf[0] * nf[1] + nf[1] * nf[2] + nf[2] * nf[0]
+    return nf, buf[: rk.value * w].reshape(rk.value, w).copy(), op.value
 
 
 def fg_type_invariant(m, n, p, ring, coeffs):

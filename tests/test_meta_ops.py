@@ -131,3 +131,26 @@ def test_scheme_key_is_invariant_under_row_order_and_sign(fg, orc):
     rng = np.random.default_rng(0)
     assert fg.fg_scheme_key(m, n, p, ZT, after[rng.permutation(7)]) == k
     assert fg.fg_scheme_key(m, n, p, ZT, orc.naive(2, 2, 2)) != k
+
+
+def test_resize_alg2_matches_oracle(fg, orc):
+    """Alg. 2 (R31): libfg and the oracle take the same decisions from
+    the same Philox words and produce byte-identical schemes, which verify; the op
+    mix follows PAPER:378 (swap 1/2; project/product/double/extend 5/50/30/15)."""
+    _, _, _, strassen = load_scheme("sec36_after.txt")
+    _, _, _, s223 = load_scheme("scheme_2x2x3_r11.txt")
+    bests = [((2, 2, 2), strassen), ((2, 2, 3), s223), ((2, 2, 1), orc.naive(2, 2, 1)),
+             ((2, 3, 2), orc.naive(2, 3, 2))]
+    starts = [((2, 2, 2), strassen), ((2, 2, 3), s223), ((3, 2, 2), orc.naive(3, 2, 2)),
+              ((2, 3, 3), orc.naive(2, 3, 3))]
+    ops = np.zeros(6, int)
+    for t in range(400):
+        fmt, c = starts[t % len(starts)]
+        got = fg.fg_resize(fmt, c, bests, 160, 0x5EED, t, t * 7 + 1, thr_resize=3 << 30)
+        ref = orc.resize(fmt, c, bests, 160, 0x5EED, t, t * 7 + 1, thr_resize=3 << 30)
+        assert got[0] == ref[0] and got[2] == ref[2] and np.array_equal(got[1], ref[1]), t
+        nf, out, op = got
+        assert orc.verify(*nf, ZT, out)[0] == 0
+        ops[op >> 1] += 1
+    assert ops[1] > 0 and ops[2] + ops[3] + ops[4] + ops[5] > 50
+    assert ops[3] > ops[4] > ops[2]             # product > double > project (50 / 30 / 5)
