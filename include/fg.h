@@ -106,6 +106,13 @@ int fg_seed_naive(fg_ctx *ctx);
    FG_E_INVALID_SCHEME, FG_E_ARG. */
 int fg_seed_pool(fg_ctx *ctx, const int8_t *coeffs, int rank, int64_t w_begin, int64_t w_end);
 
+/* Load walkers [w_begin, w_begin+count) with one scheme EACH: coeffs is count * r_cap
+   rows (row-padded), ranks[k] rows used by walker w_begin+k.  Every scheme is
+   verified and sign-normalised; each walker's best is its scheme, its step index,
+   digest and counters restart.  Used by exploratory search after a
+   Resize round.  Errors as fg_seed_pool. */
+int fg_load_walkers(fg_ctx *ctx, const int8_t *coeffs, const int32_t *ranks, int64_t w_begin, int64_t count);
+
 /* Run `steps` iterations of Algorithm 1 (reading R17) on every
    walker, Philox key = seed (R8).  Split into launches of params->phase_steps
    steps.  After the walk: the batched verifier checks every strict improvement

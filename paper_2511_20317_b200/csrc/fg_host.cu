@@ -418,6 +418,40 @@ int fg_seed_pool(fg_ctx *c, const int8_t *coeffs, int rank, int64_t w0, int64_t 
     return seed_planes(c, planes.data(), rank, w0, w1);
 }
 
+int fg_load_walkers(fg_ctx *c, const int8_t *coeffs, const int32_t *ranks, int64_t w_begin, int64_t count)
+{
+    if (!c || !coeffs || !ranks || w_begin < 0 || count < 1 || w_begin + count > c->W) return FG_E_ARG;
+    const size_t words = (size_t)FG_PLANES * c->R;
+    const int w = width_of(c->m, c->n, c->p);
+    std::vector<uint64_t> planes(words * count);
+    std::vector<fg_whdr> hdr(count);
+    for (int64_t k = 0; k < count; ++k) {
+        const int rank = ranks[k];
+        if (rank < 1 || rank > c->R) return FG_E_CAPACITY;
+        uint64_t *pl = planes.data() + k * words;
+        int rc = pack_planes(c->m, c->n, c->p, c->ring, coeffs + (size_t)k * c->R * w, rank, c->R, pl);
+        if (rc != FG_OK) return rc;
+        if (has_zero_factor(pl, c->R, rank)) return FG_E_DOMAIN;
+        int32_t ff[3];
+        rc = verify_planes(c->m, c->n, c->p, c->ring, pl, c->R, rank, ff);
+        if (rc != FG_OK) return rc;
+        if (c->ring == FG_ZT) normalize_planes(pl, c->R, rank);
+        memset(&hdr[k], 0, sizeof(fg_whdr));
+        hdr[k].r = rank;
+        hdr[k].best_r = rank;
+        hdr[k].digest = 0xcbf29ce484222325ULL;
+        hdr[k].best_adds = additions_planes(c->m, c->p, pl, c->R, rank);
+    }
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(c->d_cur + w_begin * words, planes.data(), words * count * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_best + w_begin * words, planes.data(), words * count * 8, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_hdr + w_begin, hdr.data(), sizeof(fg_whdr) * count, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (w_begin == 0 && count == c->W) c->seeded = true;
+    if (!c->seeded) return FG_OK;
+    return recompute_local_best(c);
+}
+
 int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
 {
     if (!c) return FG_E_ARG;

@@ -52,6 +52,7 @@ _sig = {
     "fg_seed_naive": (_i32, [_vp]),
     "fg_seed_pool": (_i32, [_vp, _vp, _i32, _i64, _i64]),
     "fg_walk": (_i32, [_vp, _u64, _u64, _vp]),
+    "fg_load_walkers": (_i32, [_vp, _vp, _vp, _i64, _i64]),
     "fg_verify": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
     "fg_verify_batch": (_i32, [_vp, _vp, _vp, _i64, _vp, _vp]),
     "fg_best": (_i32, [_vp, _vp, _vp, _vp, _vp]),
@@ -274,6 +275,16 @@ class FlipGraph:
         c = np.ascontiguousarray(coeffs, dtype=np.int8)
         w_end = self.W if w_end is None else w_end
         _ck(_lib.fg_seed_pool(self.ctx, _p(c), c.shape[0], w_begin, w_end), "fg_seed_pool")
+
+    def load_walkers(self, schemes, w_begin=0):
+        """One scheme per walker (list of int8 [rank, width] arrays)."""
+        k = len(schemes)
+        buf = np.zeros((k, self.R, self.width), np.int8)
+        ranks = np.zeros(k, np.int32)
+        for i, c in enumerate(schemes):
+            buf[i, : len(c)] = c
+            ranks[i] = len(c)
+        _ck(_lib.fg_load_walkers(self.ctx, _p(buf), _p(ranks), w_begin, k), "fg_load_walkers")
 
     def walk(self, steps, seed, params: fg_params | None = None):
         _ck(_lib.fg_walk(self.ctx, steps, seed, None if params is None else C.byref(params)),

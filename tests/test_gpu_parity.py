@@ -304,3 +304,24 @@ def test_best_adds_tracks_best_scheme_in_walk_mode(fg, orc):
     got = g.get_walkers()
     for k in range(0, 512, 5):
         assert got["best_adds"][k] == orc.additions(3, 3, 3, got["best"][k][: got["best_r"][k]])
+
+
+def test_load_walkers_distinct_schemes(fg, orc):
+    """fg_load_walkers (one scheme per walker, used by exploratory search) continues
+    each walker exactly like an oracle walker seeded with that scheme."""
+    schemes = []
+    for k in range(12):
+        w = orc.walker(3, 3, 3, ZT, 32, walker_id=100 + k)
+        w.seed_naive()
+        w.walk(500 + 100 * k, 9)
+        schemes.append(w.rows())
+    g = _ctx(fg, 3, 3, 3, ZT, 32, 12, base=40)
+    g.load_walkers(schemes)
+    g.walk(1200, 31)
+    got = g.get_walkers()
+    for k in range(12):
+        w = orc.walker(3, 3, 3, ZT, 32, walker_id=40 + k)
+        w.seed_rows(schemes[k])
+        w.walk(1200, 31)
+        assert w.digest == got["digest"][k] and w.r == got["r"][k]
+        assert np.array_equal(w.rows(), got["rows"][k][: w.r])
