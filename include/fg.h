@@ -234,6 +234,17 @@ int fg_resize(int *m, int *n, int *p, int ring, int8_t *coeffs, int *rank, int r
               const int32_t *bfmt, const int32_t *brank, const int8_t *const *bcoeffs, uint32_t thr_resize,
               uint64_t seed, uint64_t round, uint64_t walker_id, int *op_out);
 
+/* Z_2 -> Z_T lifting (reading R32): find signs for the nonzero
+   coefficients of a Z_2 scheme (rank rows of {0,1}) so that the Brent equations
+   hold over the integers.  Depth-first search with the first nonzero of every row's
+   u and v pinned to +1 and per-equation reachability pruning, at most
+   node_budget nodes.  FG_OK: `out` holds the lifted scheme (rank rows in {-1,0,1},
+   same support); FG_E_INVALID_SCHEME: no lift exists (search exhausted, or the
+   input is not a Z_2 scheme); FG_E_STATE: budget exhausted (no conclusion).
+   *nodes_used (may be NULL) reports the search size.  Host only. */
+int fg_lift(int m, int n, int p, const int8_t *z2, int rank, int64_t node_budget, int8_t *out,
+            int64_t *nodes_used);
+
 /* Type invariant: counts[(ru*65 + rv)*65 + rw] = number of terms whose
    U, V, W factor matrices (m x n, n x p, p x m) have ranks (ru, rv, rw) over Q;
    rank_sums = the exponents of the rank-sum polynomial.  The

@@ -126,6 +126,8 @@ int or_resize(int *m, int *n, int *p, int8_t *coeffs, int *rank, int r_cap, int 
               const int32_t *brank, const int8_t *const *bcoeffs, uint32_t thr_resize, uint64_t seed,
               uint64_t round, uint64_t walker_id, int *op_out);                 /* Alg. 2, R31 */
 
+int or_lift_exhaustive(int m, int n, int p, const int8_t *z2, int rank, int8_t *out);  /* lift.c */
+
 /* many walkers in one flat call (bench cpu baseline / tests): walker k has global
    id id_base+k, all seeded naive (or from coeffs if rank>0).  Output per walker:
    r, best_r, digest, cnt[OR_NCNT], and optionally rows/best (R*(mn+np+pm) int8). */

@@ -13,7 +13,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "liboracle.so")
-SOURCES = ["philox_bits.c", "scheme.c", "walk.c", "meta.c"]
+SOURCES = ["philox_bits.c", "scheme.c", "walk.c", "meta.c", "lift.c"]
 NCNT = 12
 CNT_NAMES = ["steps", "draws", "flips", "flip_fail", "expand_ok", "expand_reject", "merges",
              "zero_removed", "best_copies", "improvements", "reduce_calls", "verify_fail"]
@@ -94,6 +94,7 @@ class Oracle:
         lib.or_meta_extend.argtypes = [i32, i32, i32, vp, i32, vp, vp]
         lib.or_meta_merge.argtypes = [i32, i32, i32, i32, vp, i32, vp, i32, vp]
         lib.or_meta_product.argtypes = [i32, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]
+        lib.or_lift_exhaustive.argtypes = [i32, i32, i32, vp, i32, vp]
         lib.or_resize.argtypes = [vp, vp, vp, vp, vp, i32, i32, vp, vp, vp, C.c_uint32, u64, u64, u64, vp]
         lib.or_run_walkers.argtypes = [i32, i32, i32, i32, i32, i64, u64, vp, vp, i32, u64, u64,
                                        vp, i32, vp, vp, vp, vp, vp, vp]
@@ -211,6 +212,12 @@ class Oracle:
         nf = (m_.value, n_.value, p_.value)
         w = nf[0] * nf[1] + nf[1] * nf[2] + nf[2] * nf[0]
         return nf, buf[: rk.value * w].reshape(rk.value, w).copy(), op.value
+
+    def lift_exhaustive(self, m, n, p, z2):
+        c = np.ascontiguousarray(z2, dtype=np.int8)
+        out = np.zeros_like(c)
+        rc = self.lib.or_lift_exhaustive(m, n, p, _p(c), c.shape[0], _p(out))
+        return rc, (out if rc == 1 else None)
 
     def matrix_rank(self, a):
         a = np.ascontiguousarray(a, dtype=np.int8)

@@ -80,6 +80,7 @@ _sig = {
     "fg_meta_product": (_i32, [_i32, _i32, _i32, _vp, _i32, _i32, _i32, _i32, _vp, _i32, _i32, _vp]),
     "fg_resize": (_i32, [_vp, _vp, _vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _vp, C.c_uint32, _u64,
                           _u64, _u64, _vp]),
+    "fg_lift": (_i32, [_i32, _i32, _i32, _vp, _i32, _i64, _vp, _vp]),
     "fg_type_invariant": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
     "fg_scheme_key": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
 }
@@ -182,6 +183,15 @@ def fg_resize(fmt, coeffs, bests, r_cap, seed, rnd, walker_id, ring=FG_ZT, thr_r
     nf = (m_.value, n_.value, p_.value)
     w = nf[0] * nf[1] + nf[1] * nf[2] + nf[2] * nf[0]
     return nf, buf[: rk.value * w].reshape(rk.value, w).copy(), op.value
+
+
+def fg_lift(m, n, p, z2, node_budget=10_000_000):
+    """Z_2 -> Z_T lifting: (status, lifted coeffs or None, nodes)."""
+    c = np.ascontiguousarray(z2, dtype=np.int8)
+    out = np.zeros_like(c)
+    nodes = C.c_int64(0)
+    rc = _lib.fg_lift(m, n, p, _p(c), c.shape[0], node_budget, _p(out), C.byref(nodes))
+    return rc, (out if rc == 0 else None), nodes.value
 
 
 def fg_type_invariant(m, n, p, ring, coeffs):
