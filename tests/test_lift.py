@@ -38,15 +38,27 @@ def test_strassen_mod2_lifts(fg, orc):
     assert orc.lift_exhaustive(2, 2, 2, z)[0] == 1
 
 
+def _free_signs(fmt, z):
+    m, n, p = fmt
+    return int(z.sum()) - 2 * len(z)          # nonzeros minus the pinned u and v signs
+
+
 def test_lift_agrees_with_exhaustive_oracle(fg, orc):
     seen = {0: 0, 1: 0}
-    for fmt in [(2, 2, 2), (1, 2, 3), (2, 1, 3), (3, 1, 2)]:
-        for wid in range(60):
+    # Z_2 walk outputs of small formats, plus one rank-6 (1,2,3) scheme (walker 573,
+    # 4211 steps, key 3, its best) that has NO Z_T lift: 26 free signs, ~15 s of
+    # exhaustive enumeration in the oracle
+    cases = [(f, wid, 500 + wid * 13, 5, 22) for f in [(2, 2, 2), (1, 2, 3), (2, 1, 3), (3, 1, 2)]
+             for wid in range(25)]
+    cases += [((1, 2, 3), 573, 200 + 573 * 7, 3, 26)]
+    for fmt, wid, steps, key, maxfree in cases:
             w = orc.walker(*fmt, 1, 32, walker_id=wid)
             w.seed_naive()
-            w.walk(500 + wid * 13, 5)
+            w.walk(steps, key)
             for which in (0, 1):
                 z = w.rows(which)
+                if _free_signs(fmt, z) > maxfree:
+                    continue
                 ex, exout = orc.lift_exhaustive(*fmt, z)
                 if ex < 0:
                     continue
@@ -57,7 +69,7 @@ def test_lift_agrees_with_exhaustive_oracle(fg, orc):
                 else:
                     assert rc == -4
                 seen[ex] += 1
-    assert seen[1] > 100 and seen[0] >= 1            # both outcomes exercised
+    assert seen[1] > 50 and seen[0] >= 1             # both outcomes exercised
 
 
 def test_budget_and_domain(fg, orc):
