@@ -37,6 +37,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for tests")
     return ap.parse_args()
 
 
@@ -162,12 +163,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    dev = local % torch.cuda.device_count()     # one GPU per rank (modulo only for tests)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(args.dist_backend)
     stream = torch.cuda.current_stream()
     W = args.walkers or wl.walkers
-    g = fg.FlipGraph(wl.m, wl.n, wl.p, wl.ring, wl.r_cap, W, rank * W, local, stream.cuda_stream)
+    g = fg.FlipGraph(wl.m, wl.n, wl.p, wl.ring, wl.r_cap, W, rank * W, dev, stream.cuda_stream)
     sync = PoolSync(g, world)
     g.seed_naive()
     S = args.phase_steps
@@ -196,7 +201,7 @@ def main():
         phase()
     st0 = g.stats()
     r_before = g.get_walkers(rows=False)["r"].mean()
-    clocks = Clocks(local)
+    clocks = Clocks(dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -211,7 +216,8 @@ def main():
     st1 = g.stats()
     r_after = g.get_walkers(rows=False)["r"].mean()
     total_ms = sum(times)
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    t = torch.tensor([total_ms], dtype=torch.float64,
+                     device="cuda" if args.dist_backend == "nccl" else "cpu")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -251,7 +257,8 @@ def main():
             g.save_state(host.data_ptr())
             torch.cuda.synchronize()
             e_times.append(time.perf_counter() - t0)
-        te = torch.tensor([sum(e_times)], dtype=torch.float64, device="cuda")
+        te = torch.tensor([sum(e_times)], dtype=torch.float64,
+                          device="cuda" if args.dist_backend == "nccl" else "cpu")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": float(W) * S * len(e_times) * world / float(te.item()), "unit": "flip-steps/s",
