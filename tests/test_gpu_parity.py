@@ -325,3 +325,32 @@ def test_load_walkers_distinct_schemes(fg, orc):
         w.walk(1200, 31)
         assert w.digest == got["digest"][k] and w.r == got["r"][k]
         assert np.array_equal(w.rows(), got["rows"][k][: w.r])
+
+
+def test_api_errors_and_stats(fg, orc):
+    """Error paths of the ABI (no partial work): walk before seed, bad params,
+    unsupported capacity; stats accumulate; fg_get_walker agrees with the bulk call."""
+    g = _ctx(fg, 3, 3, 3, ZT, 32, 8)
+    with pytest.raises(fg.FgError) as e:
+        g.walk(10, 1)
+    assert e.value.status == -6                     # FG_E_STATE: not seeded
+    g.seed_naive()
+    with pytest.raises(fg.FgError) as e:
+        g.walk(10, 1, fg.params_default(k_flip=0))
+    assert e.value.status == -1
+    with pytest.raises(fg.FgError) as e:
+        g.walk(10, 1, fg.params_default(flags=8))
+    assert e.value.status == -1
+    with pytest.raises(fg.FgError) as e:
+        fg.FlipGraph(3, 3, 3, ZT, 600, 4, 0, 0, _stream())
+    assert e.value.status == -2
+    with pytest.raises(fg.FgError) as e:
+        g.seed_pool(orc.naive(3, 3, 3)[:5])        # does not verify
+    assert e.value.status == -4
+    g.walk(300, 2)
+    g.walk(200, 2)
+    st = g.stats()
+    assert st["steps"] == 8 * 500 and st["walk_launches"] == 2 and st["launches"] >= 4
+    got = g.get_walkers()
+    assert np.all(got["cnt"][:, 0] == 500) and np.all(got["step"] == 500)
+    assert int(got["cnt"][:, 2].sum()) == st["flips"]
