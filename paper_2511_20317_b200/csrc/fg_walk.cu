@@ -574,23 +574,25 @@ cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
 
 }  // namespace
 
-// R <= 32: the warp kernel (every factor then has <= 32 elements: the matmul
-// tensor's rank is at least max(mn, np, pm)).  33 <= R <= 512: the multi-row kernel
-// (fg_walk_multi.cu) with the narrowest factor layout that fits.
-// For R <= 32 the default is one walker per warp (this file); FG_WALK_KERNEL=h16
-// selects the two-walkers-per-warp kernel (fg_walk_h16.cu; parity-exact, measured
-// 1.82 vs 1.92 G flip-steps/s on C2, profiles/r01_ncu_walk_h16.txt).
+// R <= 32: one-word factors (Z_T <= 16 elements, Z_2 <= 32) run one walker per
+// thread (fg_walk_t1.cu); Z_T with 17..32 elements runs this file's one walker per
+// warp.  33 <= R <= 512: the multi-row kernel (fg_walk_multi.cu) with the narrowest
+// factor layout that fits.  FG_WALK_KERNEL=w32 / h16 force the one-walker-per-warp /
+// two-walkers-per-warp kernels for R <= 32 (all three are parity-exact).
 int fg_pick_kernel(int ring, int maxlen, int R)
 {
     if (R <= 32) {
         if (maxlen > 32) return FG_K_NONE;
         const char *env = getenv("FG_WALK_KERNEL");
-        const bool w32 = !(env && strcmp(env, "h16") == 0);
+        const bool h16 = env && strcmp(env, "h16") == 0;
+        const bool w32 = env && strcmp(env, "w32") == 0;
         if (ring == FG_ZT) {
-            if (w32) return maxlen <= 16 ? FG_K_W32_ZT_K16 : FG_K_W32_ZT_K32;
-            return maxlen <= 16 ? FG_K_H16_P16 : FG_K_H16_P32;
+            if (h16) return maxlen <= 16 ? FG_K_H16_P16 : FG_K_H16_P32;
+            if (maxlen > 16) return FG_K_W32_ZT_K32;
+            return w32 ? FG_K_W32_ZT_K16 : FG_K_T1_P16;
         }
-        return w32 ? FG_K_W32_Z2_K32 : FG_K_H16_Z2;
+        if (h16) return FG_K_H16_Z2;
+        return w32 ? FG_K_W32_Z2_K32 : FG_K_T1_Z2;
     }
     return fg_multi_kind(ring, maxlen, R);
 }
@@ -598,9 +600,11 @@ int fg_pick_kernel(int ring, int maxlen, int R)
 int fg_kind_for_mode(int kind)
 {
     switch (kind) {
-    case FG_K_H16_P16: return FG_K_W32_ZT_K16;
+    case FG_K_H16_P16:
+    case FG_K_T1_P16: return FG_K_W32_ZT_K16;
     case FG_K_H16_P32: return FG_K_W32_ZT_K32;
-    case FG_K_H16_Z2: return FG_K_W32_Z2_K32;
+    case FG_K_H16_Z2:
+    case FG_K_T1_Z2: return FG_K_W32_Z2_K32;
     default: return kind;
     }
 }
@@ -619,6 +623,8 @@ const char *fg_kernel_kind_name(int kind)
     case FG_K_H16_P16: return "walk_h16<P16>";
     case FG_K_H16_P32: return "walk_h16<P32>";
     case FG_K_H16_Z2: return "walk_h16<PZ2>";
+    case FG_K_T1_P16: return "walk_t1<P16>";
+    case FG_K_T1_Z2: return "walk_t1<PZ2>";
     default: return "none";
     }
 }
@@ -632,6 +638,8 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_H16_P16:
     case FG_K_H16_P32:
     case FG_K_H16_Z2: return fg_launch_walk_h16(kind, a, num_sms, st);
+    case FG_K_T1_P16:
+    case FG_K_T1_Z2: return fg_launch_walk_t1(kind, a, st);
     default: return fg_launch_walk_multi(kind, fg_multi_ns(a.R), a, num_sms, st);
     }
 }
