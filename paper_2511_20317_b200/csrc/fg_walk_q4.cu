@@ -1,0 +1,680 @@
+// fg_walk_q4.cu -- the RandomWalk kernel (Algorithm 1) for walkers
+// with at most 32 rows and one-word factors (Z_T <= 16 elements, Z_2 <= 32):
+// ONE WALKER PER QUAD (4 lanes), 8 walkers per warp.
+//
+// Why: the one-walker-per-warp kernel (fg_walk.cu) replicates per-walker scalar
+// work on 32 lanes (~420 warp instructions per walker-step); one walker per thread
+// (fg_walk_t1.cu, 90) leaves a single warp per scheduler at the C2 population
+// (16384 walkers = 512 warps on 592 SMSPs, 22% issue, profiles/r01_ncu_walk_t1.txt)
+// and lets the slowest of 32 walkers set every loop's trip count (~6 flip draws per
+// step for 2 on average).  A quad is the middle: 4x the warps, and the quad splits
+// the walker's parallel work:
+//   - Philox (R8): lane 0 computes block 0 (draw 0 + the three Bernoulli words),
+//     lanes 1-3 block 2 (draws 1-4) -- one block time per step;
+//   - try_flip (R11): lane q evaluates draw 4t+q in round t; the quad ballot picks the
+//     first valid draw, exactly the draw the sequential loop commits (1.07 rounds per
+//     walker on average instead of 2 draws);
+//   - class-mask passes, the initial mask build, best copies and the HBM loads and
+//     stores are split by row ownership: lane q owns rows l with l % 4 == q.
+// Every per-walker scalar (r, best, the step, digest, candidate totals, wneg,
+// counters) is replicated in the 4 lanes and evolves identically, so the quad's
+// control flow is uniform and every collective uses the quad mask.
+//
+// Shared memory: per warp a region of T1-style slots with stride 8 (walker w of the
+// warp at word slot*8 + w): a slot access by the 4 lanes of a quad (rows l = q mod 4,
+// slots 3l+X / l) lands in banks 8*((3q+X) mod 4) + w (resp. 8*q + w) and a
+// broadcast read of any slot in bank 8*(slot mod 4) + w -- conflict-free both ways.
+// Smem writes are done by the owning lane only; __syncwarp(quad) separates a write
+// phase from the next cross-lane read.
+//
+// Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
+// tests/test_gpu_parity.py.
+#include "fg_device.cuh"
+
+using namespace fgd;
+
+#define Q4_THREADS 128
+#define Q4_WARPS (Q4_THREADS / 32)
+#ifndef Q4_MINB
+#define Q4_MINB 4
+#endif
+
+namespace {
+
+enum : int { SF = 0, SMK = 96, SL = 192, SP = 224, SB = 256, Q4_SLOTS = 352 };
+
+__device__ __forceinline__ int nth_bit_q4(uint32_t x, uint32_t t)
+{
+    for (uint32_t k = 0; k < t; ++k) x &= x - 1u;
+    return __ffs(x) - 1;
+}
+
+template <class P>
+__global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
+{
+    typedef typename P::F F;
+    static_assert(sizeof(F) == 4, "one-word factor layouts only");
+    __shared__ uint32_t smem[Q4_WARPS][Q4_SLOTS * 8];
+    const int lane = threadIdx.x & 31;
+    const int q = lane & 3;
+    const int qb = lane & 28;
+    const unsigned qm = 0xFu << qb;
+    uint32_t *const S = smem[threadIdx.x >> 5] + (lane >> 2);
+    const int64_t wk = ((int64_t)blockIdx.x * Q4_WARPS + (threadIdx.x >> 5)) * 8 + (lane >> 2);
+    if (wk >= a.num_walkers) return;      // the whole quad
+
+#define FK(l, X) S[(SF + (l) * 3 + (X)) * 8]
+#define MK(l, X) S[(SMK + (l) * 3 + (X)) * 8]
+#define LK(l) S[(SL + (l)) * 8]
+#define PK(l) S[(SP + (l)) * 8]
+#define BK(l, X) S[(SB + (l) * 3 + (X)) * 8]
+
+    auto qsync = [&]() { __syncwarp(qm); };
+    auto qor = [&](uint32_t v) {
+        v |= __shfl_xor_sync(qm, v, 1);
+        v |= __shfl_xor_sync(qm, v, 2);
+        return v;
+    };
+    auto qsum = [&](int v) {
+        v += __shfl_xor_sync(qm, v, 1);
+        v += __shfl_xor_sync(qm, v, 2);
+        return v;
+    };
+    auto qbcast = [&](uint32_t v, int src) { return __shfl_sync(qm, v, qb | src); };
+    const uint32_t own = 0x11111111u << q;    // rows this lane owns
+    auto owner = [&](int l) -> bool { return (l & 3) == q; };
+
+    const int R = a.R;
+    const uint64_t seed = a.seed;
+    const uint32_t kf = a.k_flip;
+    const uint32_t wid = (uint32_t)(a.id_base + wk);
+    fg_whdr *hp = a.hdr + wk;
+    const uint64_t *cp = a.cur + (size_t)wk * FG_PLANES * R;
+    uint64_t *bw = a.best + (size_t)wk * FG_PLANES * R;
+
+    int r = hp->r;
+    int best = hp->best_r;
+    uint64_t step = hp->step;
+    uint64_t digest = hp->digest;
+    int best_adds = hp->best_adds;
+
+    // ---------------- load the walker and its best (own rows) ----------------
+    uint32_t wneg = 0, bwneg = 0;
+    int nnz_cur = 0;
+#pragma unroll 1
+    for (int l = q; l < 32; l += 4) {
+        F u = 0, v = 0, w = 0, bu = 0, bv = 0, bwv = 0;
+        if (l < R) {
+            if (l < r) {
+                u = P::make(cp[0 * R + l], cp[1 * R + l]);
+                v = P::make(cp[2 * R + l], cp[3 * R + l]);
+                w = P::make(cp[4 * R + l], cp[5 * R + l]);
+            }
+            if (l < best) {
+                bu = P::make(bw[0 * R + l], bw[1 * R + l]);
+                bv = P::make(bw[2 * R + l], bw[3 * R + l]);
+                bwv = P::make(bw[4 * R + l], bw[5 * R + l]);
+            }
+        }
+        nnz_cur += l < r ? P::popd(u) + P::popd(v) + P::popd(w) : 0;
+        wneg |= (uint32_t)P::first_neg(w) << l;
+        bwneg |= (uint32_t)P::first_neg(bwv) << l;
+        FK(l, 0) = u; FK(l, 1) = v; FK(l, 2) = P::abs(w);
+        BK(l, 0) = bu; BK(l, 1) = bv; BK(l, 2) = P::abs(bwv);
+    }
+    wneg = qor(wneg);
+    bwneg = qor(bwneg);
+    nnz_cur = qsum(nnz_cur);
+    qsync();
+    auto live_mask = [&]() -> uint32_t { return r >= 32 ? FULL : ((1u << r) - 1u); };
+    auto above_of = [](int l) -> uint32_t { return ~((2u << l) - 1u); };
+
+    // class masks and later counts of own rows from scratch (once per launch)
+    uint32_t nCp = 0;
+    {
+        const uint32_t live = live_mask();
+        uint32_t part = 0;
+#pragma unroll 1
+        for (int l = q; l < 32; l += 4) {
+            uint32_t lc = 0;
+#pragma unroll
+            for (int X = 0; X < 3; ++X) {
+                const uint32_t key = FK(l, X);
+                uint32_t m = 0;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) m |= (FK(j, X) == key) ? (1u << j) : 0u;
+                m = l < r ? (m & live) : 0u;
+                MK(l, X) = m;
+                lc |= (uint32_t)__popc(m & above_of(l)) << (10 * X);
+            }
+            LK(l) = lc;
+            part += lc;
+        }
+        nCp = (uint32_t)qsum((int)part);
+        qsync();
+    }
+    bool pdirty = true;    // PF stale
+    bool maybe = true;     // R15: a full reduce_all may find work
+    bool bdirty = false;   // best rows changed in this launch
+
+    auto fac = [&](int l, int X) -> F {
+        const F k = FK(l, X);
+        return (X == 2 && ((wneg >> l) & 1u)) ? P::neg(k) : k;
+    };
+    auto read_row = [&](int l) -> Row<P> {
+        Row<P> x;
+        x.u = FK(l, 0);
+        x.v = FK(l, 1);
+        const F k = FK(l, 2);
+        x.w = ((wneg >> l) & 1u) ? P::neg(k) : k;
+        return x;
+    };
+    auto two_of = [&](int l) -> uint32_t {
+        const uint32_t mu = MK(l, 0), mv = MK(l, 1), mw = MK(l, 2);
+        return ((mu & mv) | (mu & mw) | (mv & mw)) & ~(1u << l);
+    };
+    auto row_zero = [&](int l) -> bool { return P::zero(FK(l, 0)) || P::zero(FK(l, 1)) || P::zero(FK(l, 2)); };
+
+    // row l's X key becomes `key` (fresh: l was not in any X class).  Collective.
+    auto set_class = [&](int l, int X, uint32_t key, bool fresh) {
+        const uint32_t bl = 1u << l;
+        const uint32_t mo = fresh ? 0u : (MK(l, X) & ~bl);
+        qsync();                                   // old state of row l read by all
+        if (owner(l)) FK(l, X) = key;
+        uint32_t mn = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = 4 * k + q;
+            mn |= (FK(j, X) == key) ? (1u << j) : 0u;
+        }
+        mn = qor(mn) & live_mask() & ~bl;
+        const int sh = 10 * X;
+        const uint32_t one = 1u << sh;
+        for (uint32_t t = mo & own; t; t &= t - 1u) {
+            const int m = __ffs(t) - 1;
+            MK(m, X) &= ~bl;
+            if (m < l) LK(m) -= one;
+        }
+        for (uint32_t t = mn & own; t; t &= t - 1u) {
+            const int m = __ffs(t) - 1;
+            MK(m, X) |= bl;
+            if (m < l) LK(m) += one;
+        }
+        const uint32_t ab = above_of(l);
+        if (owner(l)) {
+            MK(l, X) = mn | bl;
+            LK(l) += (uint32_t)(__popc(mn & ab) - __popc(mo & ab)) << sh;
+        }
+        nCp += (uint32_t)(__popc(mn) - __popc(mo)) << sh;
+        pdirty = true;
+        qsync();
+    };
+    // store a whole (normalised) row; only changed keys pay a class update.  Collective.
+    auto write_row = [&](int l, const Row<P> &x, bool fresh) {
+        const F o0 = FK(l, 0), o1 = FK(l, 1), o2 = FK(l, 2);
+        if (fresh) {
+            qsync();
+            if (owner(l)) LK(l) = 0;
+        } else {
+            nnz_cur -= P::popd(o0) + P::popd(o1) + P::popd(o2);
+        }
+        nnz_cur += P::popd(x.u) + P::popd(x.v) + P::popd(x.w);
+        const F k0 = x.u, k1 = x.v, k2 = P::abs(x.w);
+        if (fresh || k0 != o0) set_class(l, 0, k0, fresh);
+        if (fresh || k1 != o1) set_class(l, 1, k1, fresh);
+        if (fresh || k2 != o2) set_class(l, 2, k2, fresh);
+        wneg = (wneg & ~(1u << l)) | ((uint32_t)P::first_neg(x.w) << l);
+    };
+    // factor Y of row l becomes val (actual sign); the row's other factors are
+    // normalised, so only this factor can trigger PAPER:429 (R6).  Collective.
+    auto commit_factor = [&](int l, int Y, F val) {
+        const F old = FK(l, Y);
+        nnz_cur += P::popd(val) - P::popd(old);
+        const bool fn = P::first_neg(val);
+        F key;
+        if (Y == 2) {
+            key = P::abs(val);
+            wneg = (wneg & ~(1u << l)) | ((uint32_t)fn << l);
+        } else {
+            key = fn ? P::neg(val) : val;
+            wneg ^= (uint32_t)fn << l;
+        }
+        if (key != old) set_class(l, Y, key, false);
+    };
+    auto unlink = [&](int l, int X) {
+        const uint32_t bl = 1u << l;
+        const uint32_t mo = MK(l, X) & ~bl;
+        const uint32_t one = 1u << (10 * X);
+        for (uint32_t t = mo & own; t; t &= t - 1u) {
+            const int m = __ffs(t) - 1;
+            MK(m, X) &= ~bl;
+            if (m < l) LK(m) -= one;
+        }
+        nCp -= (uint32_t)__popc(mo) << (10 * X);
+    };
+    // R14 remove(h) with the 2-entry worklist (entries == h dropped, r-1 -> h).  Collective.
+    auto remove_row = [&](int h, int &wl0, int &wl1, int &nwl) {
+        const int last = r - 1;
+        int n2 = 0, x0 = 0, x1 = 0;
+        if (nwl >= 1 && wl0 != h) { x0 = wl0; n2 = 1; }
+        if (nwl >= 2 && wl1 != h) { if (n2 == 0) x0 = wl1; else x1 = wl1; n2++; }
+        wl0 = x0; wl1 = x1; nwl = n2;
+        nnz_cur -= P::popd(FK(h, 0)) + P::popd(FK(h, 1)) + P::popd(FK(h, 2));
+        unlink(h, 0); unlink(h, 1); unlink(h, 2);
+        qsync();
+        if (h != last) {
+            const uint32_t bl = 1u << last, bh = 1u << h;
+            uint32_t lc = 0;
+            F kk[3];
+            uint32_t mos[3];
+#pragma unroll
+            for (int X = 0; X < 3; ++X) {
+                kk[X] = FK(last, X);
+                mos[X] = MK(last, X) & ~bl;
+                lc |= (uint32_t)__popc(mos[X] & above_of(h)) << (10 * X);
+            }
+            qsync();
+#pragma unroll
+            for (int X = 0; X < 3; ++X) {
+                const uint32_t one = 1u << (10 * X);
+                for (uint32_t t = mos[X] & own; t; t &= t - 1u) {
+                    const int m = __ffs(t) - 1;
+                    MK(m, X) = (MK(m, X) & ~bl) | bh;
+                    if (m > h) LK(m) -= one;
+                }
+                if (owner(h)) {
+                    FK(h, X) = kk[X];
+                    MK(h, X) = mos[X] | bh;
+                }
+            }
+            if (owner(h)) LK(h) = lc;
+            wneg = (wneg & ~bh) | (((wneg >> last) & 1u) << h);
+            if (nwl >= 1 && wl0 == last) wl0 = h;
+            if (nwl >= 2 && wl1 == last) wl1 = h;
+        }
+        if (owner(last)) LK(last) = 0;
+        wneg &= ~(1u << last);
+        r--;
+        pdirty = true;
+        qsync();
+    };
+
+    uint32_t c_draws = 0, c_flips = 0, c_red = 0, c_eok = 0, c_erej = 0, c_merge = 0, c_zero = 0,
+             c_copy = 0, c_impr = 0;
+
+    // R12: exact worklist reduction after a flip touching rows a0, b0
+    auto slow_local_reduce = [&](int a0, int b0) {
+        int wl0 = a0, wl1 = b0, nwl = 2;
+        while (nwl > 0) {
+            const int t = wl0;
+            wl0 = wl1;
+            nwl--;
+            if (t >= r) continue;
+            if (row_zero(t)) {
+                remove_row(t, wl0, wl1, nwl);
+                c_zero++;
+                continue;
+            }
+            const Row<P> rt = read_row(t);
+            Row<P> merged;
+            int j = -1;
+            for (uint32_t c = two_of(t) & live_mask(); c; c &= c - 1u) {
+                const int jj = __ffs(c) - 1;
+                if (reducible<P>(rt, read_row(jj), merged)) { j = jj; break; }
+            }
+            if (j < 0) continue;
+            const int lo = t < j ? t : j, hi = t < j ? j : t;
+            write_row(lo, merged, false);
+            c_merge++;
+            remove_row(hi, wl0, wl1, nwl);
+            if (has_zero(merged)) {
+                remove_row(lo, wl0, wl1, nwl);
+                c_zero++;
+            } else {
+                wl1 = wl0;
+                wl0 = lo;
+                nwl++;
+            }
+        }
+    };
+
+    // R15 reduce_all, exact
+    auto slow_reduce_all = [&]() {
+        for (;;) {
+            int z = -1;
+            for (int l = 0; l < r; ++l)
+                if (row_zero(l)) { z = l; break; }
+            if (z >= 0) {
+                int n0 = 0, x0 = 0, x1 = 0;
+                remove_row(z, x0, x1, n0);
+                c_zero++;
+                continue;
+            }
+            bool merged_any = false;
+            for (int i = 0; i < r && !merged_any; ++i) {
+                const uint32_t c0 = two_of(i) & above_of(i) & live_mask();
+                if (!c0) continue;
+                const Row<P> ri = read_row(i);
+                for (uint32_t c = c0; c; c &= c - 1u) {
+                    const int j = __ffs(c) - 1;
+                    Row<P> merged;
+                    if (!reducible<P>(ri, read_row(j), merged)) continue;
+                    write_row(i, merged, false);
+                    c_merge++;
+                    int n0 = 0, x0 = 0, x1 = 0;
+                    remove_row(j, x0, x1, n0);
+                    if (has_zero(merged)) {
+                        remove_row(i, x0, x1, n0);
+                        c_zero++;
+                    }
+                    merged_any = true;
+                    break;
+                }
+            }
+            if (!merged_any) break;
+        }
+    };
+
+    // R16 expand (plus / split), words from Philox block 1 of this step.  Collective.
+    auto expand = [&]() -> bool {
+        if (r < 2 || r + 1 > R) return false;
+        uint32_t b0, b1, b2, b3;
+        philox_block(seed, step, wid, 1u, b0, b1, b2, b3);
+        const bool plus = b0 < 0x80000000u;
+        const int i = (int)__umulhi(b1, (uint32_t)r);
+        int j = (int)__umulhi(b2, (uint32_t)(r - 1));
+        j += (j >= i);
+        const int perm = (int)__umulhi(b3, 6u);
+        // PERM = (U,V,W),(U,W,V),(V,U,W),(V,W,U),(W,U,V),(W,V,U)
+        const int A = perm >> 1;
+        const int B = (1161 >> (2 * perm)) & 3;
+        const int Cr = 3 - A - B;
+        Row<P> ri = read_row(i), rj = read_row(j);
+        const F ai = get(ri, A), aj = get(rj, A), bi = get(ri, B), bj = get(rj, B);
+        const F ci = get(ri, Cr), cj = get(rj, Cr);
+        bool ok = true;
+        Row<P> rn;
+        rn.u = rn.v = rn.w = 0;
+        if (plus) {
+            if (!distinct<P>(ai, aj) || !distinct<P>(bi, bj) || !distinct<P>(ci, cj)) return false;
+            const F t1 = P::add(bi, bj, ok);      // v_i + v_j
+            const F t2 = P::sub(cj, ci, ok);      // w_j - w_i
+            const F t3 = P::sub(aj, ai, ok);      // u_j - u_i
+            if (!ok) return false;
+            set(ri, B, t1, true);
+            set(rj, A, ai, true);
+            set(rj, Cr, t2, true);
+            set(rn, A, t3, true);
+            set(rn, B, bj, true);
+            set(rn, Cr, cj, true);
+            normalize<P>(ri);
+            normalize<P>(rj);
+            normalize<P>(rn);
+            write_row(i, ri, false);
+            write_row(j, rj, false);
+        } else {
+            if (!distinct<P>(ai, aj)) return false;
+            const F t3 = P::sub(ai, aj, ok);      // u_i - u_j
+            if (!ok) return false;
+            set(ri, A, aj, true);
+            set(rn, A, t3, true);
+            set(rn, B, bi, true);
+            set(rn, Cr, ci, true);
+            normalize<P>(ri);
+            normalize<P>(rn);
+            write_row(i, ri, false);
+        }
+        r++;
+        write_row(r - 1, rn, true);
+        maybe = true;
+        return true;
+    };
+
+    // best copy of own rows into shared memory; HBM once per launch
+    auto copy_best = [&]() {
+        for (int l = q; l < r; l += 4) {
+            BK(l, 0) = FK(l, 0);
+            BK(l, 1) = FK(l, 1);
+            BK(l, 2) = FK(l, 2);
+        }
+        bwneg = wneg;
+        bdirty = true;
+    };
+    // R19 verify queue entry: the current rows (== the new best), plane layout
+    auto enqueue_verify = [&]() {
+        unsigned slot = 0;
+        if (q == 0) slot = atomicAdd(a.q_count, 1u);
+        slot = qbcast(slot, 0);
+        if (slot < a.q_cap) {
+            uint64_t *dst = a.q_planes + (size_t)slot * FG_PLANES * R;
+            for (int l = q; l < R; l += 4) {
+                const bool lv = l < r;
+                const F u = lv ? FK(l, 0) : 0, v = lv ? FK(l, 1) : 0, w = lv ? fac(l, 2) : 0;
+                dst[0 * R + l] = P::dig(u); dst[1 * R + l] = P::sgn(u);
+                dst[2 * R + l] = P::dig(v); dst[3 * R + l] = P::sgn(v);
+                dst[4 * R + l] = P::dig(w); dst[5 * R + l] = P::sgn(w);
+            }
+            if (q == 0) {
+                fg_qmeta qm_;
+                qm_.walker = wk; qm_.step = step; qm_.rank = r; qm_.ok = -1;
+                qm_.ff[0] = qm_.ff[1] = qm_.ff[2] = -1; qm_.pad = 0;
+                a.q_meta[slot] = qm_;
+            }
+        } else if (q == 0) {
+            atomicAdd(a.q_overflow, 1u);
+            hp->pad |= 1;
+        }
+    };
+
+    const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
+#pragma unroll 1
+    for (uint32_t it = 0; it < nsteps; ++it, ++step) {
+        // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1-3 block 2 (draws 1-4)
+        uint32_t cb = q == 0 ? 0u : 2u;
+        uint32_t c0, c1, c2, c3;
+        philox_block(seed, step, wid, cb, c0, c1, c2, c3);
+        const uint32_t bern = qbcast(q == 0 ? ((c1 < a.thr_eq ? 1u : 0u) | (c2 < a.thr_reduce ? 2u : 0u) |
+                                               (c3 < a.thr_expand ? 4u : 0u))
+                                            : 0u,
+                                     0);
+        uint32_t flags = 0;
+        int alpha = 0, beta = 0;
+        uint32_t draws = 0;
+        bool ok = false;
+        const uint32_t nU = nCp & 1023u, nV = (nCp >> 10) & 1023u, nW = nCp >> 20;
+        const uint32_t nC = nU + nV + nW;
+        int e_Y = 0, e_Z = 0;
+        F e_ny = 0, e_nz = 0;
+        if (nC) {
+            if (pdirty) {
+                uint32_t acc = 0;
+#pragma unroll
+                for (int l = 0; l < 32; ++l) {
+                    const uint32_t v = LK(l);
+                    if ((l & 3) == q) PK(l) = acc;
+                    acc += v;
+                }
+                pdirty = false;
+                qsync();
+            }
+#pragma unroll 1
+            for (uint32_t t = 0; 4u * t < kf; ++t) {
+                const uint32_t att = 4u * t + (uint32_t)q;
+                uint32_t x;
+                if (t == 0) {
+                    x = q <= 1 ? c0 : (q == 2 ? c1 : c2);
+                } else {
+                    const uint32_t slot = 7u + att, blk = slot >> 2;
+                    if (blk != cb) {
+                        philox_block(seed, step, wid, blk, c0, c1, c2, c3);
+                        cb = blk;
+                    }
+                    const uint32_t wsel = slot & 3u;
+                    x = wsel == 0 ? c0 : (wsel == 1 ? c1 : (wsel == 2 ? c2 : c3));
+                }
+                // ---- R11 draw: k uniform over 4|C| (R9), candidate k>>2 in (X, i, j) order ----
+                const uint32_t k = __umulhi(x, 4u * nC);
+                const uint32_t idx = k >> 2;
+                const int d = k & 1, e = (k >> 1) & 1;
+                const uint32_t g1 = idx >= nU, g2 = idx >= nU + nV;
+                const int X = (int)(g1 + g2);
+                const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
+                const int sh = 10 * X;
+                const uint32_t fm = 1023u << sh, qs = qq << sh;
+                int i = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const uint32_t v = PK(i + st) & fm;
+                    i += (v <= qs) ? st : 0;
+                }
+                const uint32_t ex_i = (PK(i) >> sh) & 1023u;
+                const uint32_t mm = MK(i, X) & above_of(i);
+                const int j = nth_bit_q4(mm, qq - ex_i);
+                const int al = d ? j : i, be = d ? i : j;
+                // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e
+                const uint32_t yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
+                const int Y = yz & 3, Z = yz >> 2;
+                const bool sneg = P::RING == FG_ZT && X == 2 && (((wneg >> al) ^ (wneg >> be)) & 1u);
+                const F yb = fac(be, Y);
+                bool v = att < kf;
+                const F ny = P::add(fac(al, Y), sneg ? P::neg(yb) : yb, v);   // y_a + s y_b
+                const F nz = P::sub(fac(be, Z), fac(al, Z), v);             // z_b - z_a
+                const uint32_t bal = (__ballot_sync(qm, v) >> qb) & 15u;
+                if (bal) {
+                    const int src = __ffs(bal) - 1;
+                    const uint32_t info = qbcast((uint32_t)(al | (be << 8) | (Y << 16) | (Z << 18)), src);
+                    e_ny = qbcast(ny, src);
+                    e_nz = qbcast(nz, src);
+                    alpha = info & 255;
+                    beta = (info >> 8) & 255;
+                    e_Y = (info >> 16) & 3;
+                    e_Z = (info >> 18) & 3;
+                    draws = 4u * t + (uint32_t)src + 1u;
+                    ok = true;
+                    break;
+                }
+            }
+            if (!ok) draws = kf;
+        }
+        c_draws += draws;
+
+        if (!ok) {
+            // expand; continue
+            const bool ex = expand();
+            c_eok += ex;
+            c_erej += !ex;
+            flags |= 2u | (ex ? 64u : 0u);
+            alpha = beta = 0;
+        } else {
+            c_flips++;
+            flags |= 1u;
+            commit_factor(alpha, e_Y, e_ny);
+            commit_factor(beta, e_Z, e_nz);
+            // ---- R12 local reduction (exact skip through the masks) ----
+            if (P::zero(e_ny) || P::zero(e_nz) || two_of(alpha) || two_of(beta)) slow_local_reduce(alpha, beta);
+            // ---- PAPER:310-313 acceptance ----
+            const bool strict = r < best;
+            if (strict || (r == best && (bern & 1u))) {
+                best = r;
+                best_adds = nnz_cur - 2 * r - a.mp;
+                c_copy++;
+                flags |= 4u;
+                copy_best();
+                if (strict) {
+                    flags |= 8u;
+                    c_impr++;
+                    enqueue_verify();
+                }
+            }
+            // ---- PAPER:315-317 reduce (R15) ----
+            if (bern & 2u) {
+                c_red++;
+                flags |= 16u;
+                if (maybe) {
+                    slow_reduce_all();
+                    maybe = false;
+                }
+            }
+            // ---- PAPER:319-321 expand ----
+            if ((bern & 4u) && r <= best + a.slack) {
+                const bool ex = expand();
+                flags |= 32u | (ex ? 64u : 0u);
+                c_eok += ex;
+                c_erej += !ex;
+            }
+        }
+        // ---- digest ----
+        const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)best << 10) | ((uint64_t)flags << 20) |
+                            ((uint64_t)alpha << 32) | ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
+        digest = (digest ^ ev) * 0x100000001b3ULL;
+        digest ^= digest >> 32;
+    }
+
+    // ---------------- store own rows (and the best if it changed) ----------------
+    uint64_t *cw = a.cur + (size_t)wk * FG_PLANES * R;
+    int best_nnz = 0;
+    for (int l = q; l < R; l += 4) {
+        const bool lv = l < r;
+        const F u = lv ? FK(l, 0) : 0, v = lv ? FK(l, 1) : 0, w = lv ? fac(l, 2) : 0;
+        cw[0 * R + l] = P::dig(u); cw[1 * R + l] = P::sgn(u);
+        cw[2 * R + l] = P::dig(v); cw[3 * R + l] = P::sgn(v);
+        cw[4 * R + l] = P::dig(w); cw[5 * R + l] = P::sgn(w);
+        const bool lb = l < best;
+        const F bu = lb ? BK(l, 0) : 0, bv = lb ? BK(l, 1) : 0, bk = lb ? BK(l, 2) : 0;
+        const F bwv = ((bwneg >> l) & 1u) ? P::neg(bk) : bk;
+        best_nnz += P::popd(bu) + P::popd(bv) + P::popd(bwv);
+        if (bdirty) {
+            bw[0 * R + l] = P::dig(bu); bw[1 * R + l] = P::sgn(bu);
+            bw[2 * R + l] = P::dig(bv); bw[3 * R + l] = P::sgn(bv);
+            bw[4 * R + l] = P::dig(bwv); bw[5 * R + l] = P::sgn(bwv);
+        }
+    }
+    best_nnz = qsum(best_nnz);
+    if (q == 0) {
+        hp->r = r;
+        hp->best_r = best;
+        hp->step = step;
+        hp->digest = digest;
+        hp->best_adds = best_adds;
+        hp->cnt[FG_CNT_STEPS] += a.steps;
+        hp->cnt[FG_CNT_DRAWS] += c_draws;
+        hp->cnt[FG_CNT_FLIPS] += c_flips;
+        hp->cnt[FG_CNT_FLIP_FAIL] += a.steps - c_flips;
+        hp->cnt[FG_CNT_EXPAND_OK] += c_eok;
+        hp->cnt[FG_CNT_EXPAND_REJECT] += c_erej;
+        hp->cnt[FG_CNT_MERGES] += c_merge;
+        hp->cnt[FG_CNT_ZERO_REMOVED] += c_zero;
+        hp->cnt[FG_CNT_BEST_COPIES] += c_copy;
+        hp->cnt[FG_CNT_IMPROVEMENTS] += c_impr;
+        hp->cnt[FG_CNT_REDUCE_CALLS] += c_red;
+        int adds = best_nnz - 2 * best - a.mp;
+        if (adds < 0) adds = 0;
+        atomicMin(a.best_key, ((unsigned long long)best << 54) | ((unsigned long long)adds << 36) |
+                                  (unsigned long long)wk);
+    }
+#undef FK
+#undef MK
+#undef LK
+#undef PK
+#undef BK
+}
+
+template <class P>
+cudaError_t launch_q4(const WalkArgs &a, cudaStream_t st)
+{
+    const int64_t per_block = Q4_WARPS * 8;
+    const int64_t blocks = (a.num_walkers + per_block - 1) / per_block;
+    walk_q4<P><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, cudaStream_t st)
+{
+    switch (kind) {
+    case FG_K_Q4_P16: return launch_q4<P16>(a, st);
+    case FG_K_Q4_Z2: return launch_q4<PZ2>(a, st);
+    default: return cudaErrorInvalidValue;
+    }
+}
