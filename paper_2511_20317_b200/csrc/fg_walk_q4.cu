@@ -29,6 +29,7 @@
 //
 // Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
 // tests/test_gpu_parity.py.
+#include <type_traits>
 #include "fg_device.cuh"
 
 using namespace fgd;
@@ -60,8 +61,11 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     const int qb = lane & 28;
     const unsigned qm = 0xFu << qb;
     uint32_t *const S = smem[threadIdx.x >> 5] + (lane >> 2);
-    const int64_t wk = ((int64_t)blockIdx.x * Q4_WARPS + (threadIdx.x >> 5)) * 8 + (lane >> 2);
-    if (wk >= a.num_walkers) return;      // the whole quad
+    const int64_t wk_raw = ((int64_t)blockIdx.x * Q4_WARPS + (threadIdx.x >> 5)) * 8 + (lane >> 2);
+    // a quad past the last walker stays in the warp (r = 0, no stores) so the main
+    // loop's full-warp collectives see every lane
+    const bool valid = wk_raw < a.num_walkers;
+    const int64_t wk = valid ? wk_raw : 0;
 
 #define FK(l, X) S[(SF + (l) * 3 + (X)) * 8]
 #define MK(l, X) S[(SMK + (l) * 3 + (X)) * 8]
@@ -92,8 +96,8 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     const uint64_t *cp = a.cur + (size_t)wk * FG_PLANES * R;
     uint64_t *bw = a.best + (size_t)wk * FG_PLANES * R;
 
-    int r = hp->r;
-    int best = hp->best_r;
+    int r = valid ? hp->r : 0;
+    int best = valid ? hp->best_r : 0;
     uint64_t step = hp->step;
     uint64_t digest = hp->digest;
     int best_adds = hp->best_adds;
@@ -175,39 +179,44 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     };
     auto row_zero = [&](int l) -> bool { return P::zero(FK(l, 0)) || P::zero(FK(l, 1)) || P::zero(FK(l, 2)); };
 
-    // row l's X key becomes `key` (fresh: l was not in any X class).  Collective.
-    auto set_class = [&](int l, int X, uint32_t key, bool fresh) {
+    // row l's X key becomes `key` (fresh: l was not in any X class).  Collective over
+    // the quad (wtag false) or the whole warp (wtag true: every quad calls it, `act`
+    // says whether this quad's update is real).
+    auto set_class = [&](auto wtag, int l, int X, uint32_t key, bool fresh, bool act) {
+        constexpr bool WARP = decltype(wtag)::value;
+        const unsigned msk = WARP ? FULL : qm;
         const uint32_t bl = 1u << l;
-        const uint32_t mo = fresh ? 0u : (MK(l, X) & ~bl);
-        qsync();                                   // old state of row l read by all
-        if (owner(l)) FK(l, X) = key;
+        const uint32_t mo = (act && !fresh) ? (MK(l, X) & ~bl) : 0u;
+        __syncwarp(msk);                           // old state of row l read by all
+        if (act && owner(l)) FK(l, X) = key;
         uint32_t mn = 0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int j = 4 * k + q;
             mn |= (FK(j, X) == key) ? (1u << j) : 0u;
         }
-        mn = qor(mn) & live_mask() & ~bl;
+        mn |= __shfl_xor_sync(msk, mn, 1);
+        mn |= __shfl_xor_sync(msk, mn, 2);
+        mn = act ? (mn & live_mask() & ~bl) : 0u;
         const int sh = 10 * X;
         const uint32_t one = 1u << sh;
-        for (uint32_t t = mo & own; t; t &= t - 1u) {
+        for (uint32_t t = (mo | mn) & own; t; t &= t - 1u) {
             const int m = __ffs(t) - 1;
-            MK(m, X) &= ~bl;
-            if (m < l) LK(m) -= one;
+            const bool was = (mo >> m) & 1u;
+            const uint32_t mk = MK(m, X);
+            MK(m, X) = was ? (mk & ~bl) : (mk | bl);
+            if (m < l) LK(m) += was ? (0u - one) : one;
         }
-        for (uint32_t t = mn & own; t; t &= t - 1u) {
-            const int m = __ffs(t) - 1;
-            MK(m, X) |= bl;
-            if (m < l) LK(m) += one;
+        if (act) {
+            const uint32_t ab = above_of(l);
+            if (owner(l)) {
+                MK(l, X) = mn | bl;
+                LK(l) += (uint32_t)(__popc(mn & ab) - __popc(mo & ab)) << sh;
+            }
+            nCp += (uint32_t)(__popc(mn) - __popc(mo)) << sh;
+            pdirty = true;
         }
-        const uint32_t ab = above_of(l);
-        if (owner(l)) {
-            MK(l, X) = mn | bl;
-            LK(l) += (uint32_t)(__popc(mn & ab) - __popc(mo & ab)) << sh;
-        }
-        nCp += (uint32_t)(__popc(mn) - __popc(mo)) << sh;
-        pdirty = true;
-        qsync();
+        __syncwarp(msk);
     };
     // store a whole (normalised) row; only changed keys pay a class update.  Collective.
     auto write_row = [&](int l, const Row<P> &x, bool fresh) {
@@ -220,26 +229,24 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         }
         nnz_cur += P::popd(x.u) + P::popd(x.v) + P::popd(x.w);
         const F k0 = x.u, k1 = x.v, k2 = P::abs(x.w);
-        if (fresh || k0 != o0) set_class(l, 0, k0, fresh);
-        if (fresh || k1 != o1) set_class(l, 1, k1, fresh);
-        if (fresh || k2 != o2) set_class(l, 2, k2, fresh);
+        if (fresh || k0 != o0) set_class(std::false_type{}, l, 0, k0, fresh, true);
+        if (fresh || k1 != o1) set_class(std::false_type{}, l, 1, k1, fresh, true);
+        if (fresh || k2 != o2) set_class(std::false_type{}, l, 2, k2, fresh, true);
         wneg = (wneg & ~(1u << l)) | ((uint32_t)P::first_neg(x.w) << l);
     };
-    // factor Y of row l becomes val (actual sign); the row's other factors are
-    // normalised, so only this factor can trigger PAPER:429 (R6).  Collective.
-    auto commit_factor = [&](int l, int Y, F val) {
+    // factor Y of row l becomes val (actual sign) if `act`; the row's other factors
+    // are normalised, so only this factor can trigger PAPER:429 (R6).  Whole-warp
+    // collective (called by every quad on the main path).
+    auto commit_factor = [&](bool act, int l, int Y, F val) {
         const F old = FK(l, Y);
-        nnz_cur += P::popd(val) - P::popd(old);
         const bool fn = P::first_neg(val);
-        F key;
-        if (Y == 2) {
-            key = P::abs(val);
-            wneg = (wneg & ~(1u << l)) | ((uint32_t)fn << l);
-        } else {
-            key = fn ? P::neg(val) : val;
-            wneg ^= (uint32_t)fn << l;
+        const F key = (Y == 2 || !fn) ? (Y == 2 ? P::abs(val) : val) : P::neg(val);
+        if (act) {
+            nnz_cur += P::popd(val) - P::popd(old);
+            if (Y == 2) wneg = (wneg & ~(1u << l)) | ((uint32_t)fn << l);
+            else wneg ^= (uint32_t)fn << l;
         }
-        if (key != old) set_class(l, Y, key, false);
+        set_class(std::true_type{}, l, Y, key, false, act && key != old);
     };
     auto unlink = [&](int l, int X) {
         const uint32_t bl = 1u << l;
@@ -469,14 +476,13 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
 #pragma unroll 1
     for (uint32_t it = 0; it < nsteps; ++it, ++step) {
+        __syncwarp();
         // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1-3 block 2 (draws 1-4)
         uint32_t cb = q == 0 ? 0u : 2u;
         uint32_t c0, c1, c2, c3;
         philox_block(seed, step, wid, cb, c0, c1, c2, c3);
-        const uint32_t bern = qbcast(q == 0 ? ((c1 < a.thr_eq ? 1u : 0u) | (c2 < a.thr_reduce ? 2u : 0u) |
-                                               (c3 < a.thr_expand ? 4u : 0u))
-                                            : 0u,
-                                     0);
+        const uint32_t bern = __shfl_sync(FULL, (c1 < a.thr_eq ? 1u : 0u) | (c2 < a.thr_reduce ? 2u : 0u) |
+                                                    (c3 < a.thr_expand ? 4u : 0u), qb);
         uint32_t flags = 0;
         int alpha = 0, beta = 0;
         uint32_t draws = 0;
@@ -485,78 +491,91 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         const uint32_t nC = nU + nV + nW;
         int e_Y = 0, e_Z = 0;
         F e_ny = 0, e_nz = 0;
-        if (nC) {
-            if (pdirty) {
-                uint32_t acc = 0;
+        // R10 row prefix of the later counts (packed 3 x 10 bits), quad scan per row group
+        if (__any_sync(FULL, nC != 0 && pdirty)) {
+            uint32_t base = 0;
 #pragma unroll
-                for (int l = 0; l < 32; ++l) {
-                    const uint32_t v = LK(l);
-                    if ((l & 3) == q) PK(l) = acc;
-                    acc += v;
-                }
-                pdirty = false;
-                qsync();
+            for (int k = 0; k < 8; ++k) {
+                const uint32_t v = LK(4 * k + q);
+                uint32_t sc = v;
+                uint32_t t = __shfl_up_sync(FULL, sc, 1, 4);
+                sc += q >= 1 ? t : 0u;
+                t = __shfl_up_sync(FULL, sc, 2, 4);
+                sc += q >= 2 ? t : 0u;
+                const uint32_t tot = __shfl_sync(FULL, sc, 3, 4);
+                PK(4 * k + q) = base + sc - v;
+                base += tot;
             }
-#pragma unroll 1
-            for (uint32_t t = 0; 4u * t < kf; ++t) {
-                const uint32_t att = 4u * t + (uint32_t)q;
-                uint32_t x;
-                if (t == 0) {
-                    x = q <= 1 ? c0 : (q == 2 ? c1 : c2);
-                } else {
-                    const uint32_t slot = 7u + att, blk = slot >> 2;
-                    if (blk != cb) {
-                        philox_block(seed, step, wid, blk, c0, c1, c2, c3);
-                        cb = blk;
-                    }
-                    const uint32_t wsel = slot & 3u;
-                    x = wsel == 0 ? c0 : (wsel == 1 ? c1 : (wsel == 2 ? c2 : c3));
-                }
-                // ---- R11 draw: k uniform over 4|C| (R9), candidate k>>2 in (X, i, j) order ----
-                const uint32_t k = __umulhi(x, 4u * nC);
-                const uint32_t idx = k >> 2;
-                const int d = k & 1, e = (k >> 1) & 1;
-                const uint32_t g1 = idx >= nU, g2 = idx >= nU + nV;
-                const int X = (int)(g1 + g2);
-                const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
-                const int sh = 10 * X;
-                const uint32_t fm = 1023u << sh, qs = qq << sh;
-                int i = 0;
-#pragma unroll
-                for (int st = 16; st >= 1; st >>= 1) {
-                    const uint32_t v = PK(i + st) & fm;
-                    i += (v <= qs) ? st : 0;
-                }
-                const uint32_t ex_i = (PK(i) >> sh) & 1023u;
-                const uint32_t mm = MK(i, X) & above_of(i);
-                const int j = nth_bit_q4(mm, qq - ex_i);
-                const int al = d ? j : i, be = d ? i : j;
-                // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e
-                const uint32_t yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
-                const int Y = yz & 3, Z = yz >> 2;
-                const bool sneg = P::RING == FG_ZT && X == 2 && (((wneg >> al) ^ (wneg >> be)) & 1u);
-                const F yb = fac(be, Y);
-                bool v = att < kf;
-                const F ny = P::add(fac(al, Y), sneg ? P::neg(yb) : yb, v);   // y_a + s y_b
-                const F nz = P::sub(fac(be, Z), fac(al, Z), v);             // z_b - z_a
-                const uint32_t bal = (__ballot_sync(qm, v) >> qb) & 15u;
-                if (bal) {
-                    const int src = __ffs(bal) - 1;
-                    const uint32_t info = qbcast((uint32_t)(al | (be << 8) | (Y << 16) | (Z << 18)), src);
-                    e_ny = qbcast(ny, src);
-                    e_nz = qbcast(nz, src);
-                    alpha = info & 255;
-                    beta = (info >> 8) & 255;
-                    e_Y = (info >> 16) & 3;
-                    e_Z = (info >> 18) & 3;
-                    draws = 4u * t + (uint32_t)src + 1u;
-                    ok = true;
-                    break;
-                }
-            }
-            if (!ok) draws = kf;
+            pdirty = false;
+            __syncwarp();
         }
+        // R11 try_flip: round t, lane q evaluates draw 4t+q; every quad of the warp
+        // runs the rounds until the last one has its flip (full-warp ballots)
+        bool searching = nC != 0;
+#pragma unroll 1
+        for (uint32_t t = 0; __any_sync(FULL, searching && 4u * t < kf); ++t) {
+            const uint32_t att = 4u * t + (uint32_t)q;
+            uint32_t x;
+            if (t == 0) {
+                x = q <= 1 ? c0 : (q == 2 ? c1 : c2);
+            } else {
+                const uint32_t slot = 7u + att, blk = slot >> 2;
+                if (blk != cb) {
+                    philox_block(seed, step, wid, blk, c0, c1, c2, c3);
+                    cb = blk;
+                }
+                const uint32_t wsel = slot & 3u;
+                x = wsel == 0 ? c0 : (wsel == 1 ? c1 : (wsel == 2 ? c2 : c3));
+            }
+            // ---- R11 draw: k uniform over 4|C| (R9), candidate k>>2 in (X, i, j) order ----
+            const uint32_t k = __umulhi(x, 4u * nC);
+            const uint32_t idx = k >> 2;
+            const int d = k & 1, e = (k >> 1) & 1;
+            const uint32_t g1 = idx >= nU, g2 = idx >= nU + nV;
+            const int X = (int)(g1 + g2);
+            const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
+            const int sh = 10 * X;
+            const uint32_t fm = 1023u << sh, qs = qq << sh;
+            int i = 0;
+#pragma unroll
+            for (int st = 16; st >= 1; st >>= 1) {
+                const uint32_t v = PK(i + st) & fm;
+                i += (v <= qs) ? st : 0;
+            }
+            const uint32_t ex_i = (PK(i) >> sh) & 1023u;
+            const uint32_t mm = MK(i, X) & above_of(i);
+            const int j = nth_bit_q4(mm, qq - ex_i) & 31;     // (& 31: quads not searching)
+            const int al = d ? j : i, be = d ? i : j;
+            // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e
+            const uint32_t yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
+            const int Y = yz & 3, Z = yz >> 2;
+            const bool sneg = P::RING == FG_ZT && X == 2 && (((wneg >> al) ^ (wneg >> be)) & 1u);
+            const F yb = fac(be, Y);
+            bool v = searching && att < kf;
+            const F ny = P::add(fac(al, Y), sneg ? P::neg(yb) : yb, v);   // y_a + s y_b
+            const F nz = P::sub(fac(be, Z), fac(al, Z), v);             // z_b - z_a
+            const uint32_t bal = (__ballot_sync(FULL, v) >> qb) & 15u;
+            const int src = bal ? __ffs(bal) - 1 : 0;
+            const uint32_t info = __shfl_sync(FULL, (uint32_t)(al | (be << 8) | (Y << 16) | (Z << 18)), qb | src);
+            const F wny = __shfl_sync(FULL, ny, qb | src);
+            const F wnz = __shfl_sync(FULL, nz, qb | src);
+            if (bal) {
+                alpha = info & 255;
+                beta = (info >> 8) & 255;
+                e_Y = (info >> 16) & 3;
+                e_Z = (info >> 18) & 3;
+                e_ny = wny;
+                e_nz = wnz;
+                draws = 4u * t + (uint32_t)src + 1u;
+                ok = true;
+                searching = false;
+            }
+        }
+        if (nC && !ok) draws = kf;
         c_draws += draws;
+        // commit the flip (every quad takes part; `ok` gates the update)
+        commit_factor(ok, alpha, e_Y, e_ny);
+        commit_factor(ok, beta, e_Z, e_nz);
 
         if (!ok) {
             // expand; continue
@@ -568,8 +587,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         } else {
             c_flips++;
             flags |= 1u;
-            commit_factor(alpha, e_Y, e_ny);
-            commit_factor(beta, e_Z, e_nz);
             // ---- R12 local reduction (exact skip through the masks) ----
             if (P::zero(e_ny) || P::zero(e_nz) || two_of(alpha) || two_of(beta)) slow_local_reduce(alpha, beta);
             // ---- PAPER:310-313 acceptance ----
@@ -613,7 +630,7 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     // ---------------- store own rows (and the best if it changed) ----------------
     uint64_t *cw = a.cur + (size_t)wk * FG_PLANES * R;
     int best_nnz = 0;
-    for (int l = q; l < R; l += 4) {
+    for (int l = q; l < R && valid; l += 4) {
         const bool lv = l < r;
         const F u = lv ? FK(l, 0) : 0, v = lv ? FK(l, 1) : 0, w = lv ? fac(l, 2) : 0;
         cw[0 * R + l] = P::dig(u); cw[1 * R + l] = P::sgn(u);
@@ -630,7 +647,7 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         }
     }
     best_nnz = qsum(best_nnz);
-    if (q == 0) {
+    if (q == 0 && valid) {
         hp->r = r;
         hp->best_r = best;
         hp->step = step;
