@@ -1,0 +1,98 @@
+"""Every R <= 32 walk kernel against the CPU oracle (FG_WALK_KERNEL selects it at
+fg_create): one walker per warp (w32), two per warp (h16), one per thread (t1) and
+one per quad (q4, the default).  Same bar as test_gpu_parity.py: bit-exact final and
+best schemes, ranks, counters and the per-step event digest.
+
+Walker counts that are not multiples of 8 / 32 exercise the tail quads and warps.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import Oracle
+from paper_2511_20317_b200.inputs import WORKLOADS, sample_walkers
+
+pytestmark = pytest.mark.gpu
+ZT, Z2 = 0, 1
+KERNELS = {"w32": "walk_w32", "h16": "walk_h16", "t1": "walk_t1", "q4": "walk_q4"}
+
+
+@pytest.fixture(scope="module")
+def fg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2511_20317_b200 import fg as mod
+    return mod
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+def _ctx(fg, kernel, m, n, p, ring, R, W):
+    import torch
+    old = os.environ.get("FG_WALK_KERNEL")
+    os.environ["FG_WALK_KERNEL"] = kernel
+    try:
+        g = fg.FlipGraph(m, n, p, ring, R, W, 0, 0, torch.cuda.current_stream().cuda_stream)
+    finally:
+        if old is None:
+            del os.environ["FG_WALK_KERNEL"]
+        else:
+            os.environ["FG_WALK_KERNEL"] = old
+    assert g.kernel_name.startswith(KERNELS[kernel]), g.kernel_name
+    return g
+
+
+def _check(got, ref, ids):
+    for k in ("r", "best_r", "digest", "cnt", "rows", "best"):
+        g = got[k][ids] if ids is not None else got[k]
+        assert np.array_equal(g, ref[k]), f"{k} differs"
+
+
+@pytest.mark.parametrize("ring", [ZT, Z2])
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_kernel_c1_all_walkers(fg, orc, kernel, ring):
+    """(2,2,2) naive -> 7, 61 walkers (a partial last quad / warp), 20000 steps."""
+    W, steps, seed = 61, 20000, WORKLOADS["c1_222_zt"].seed + 7
+    g = _ctx(fg, kernel, 2, 2, 2, ring, 32, W)
+    g.seed_naive()
+    g.walk(steps, seed)
+    got = g.get_walkers()
+    ref = orc.run_walkers(2, 2, 2, ring, 32, W, 0, steps, seed)
+    _check(got, ref, None)
+    st = g.stats()
+    assert st["verify_fail"] == 0
+
+
+@pytest.mark.parametrize("ring", [ZT, Z2])
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_kernel_c2_sampled(fg, orc, kernel, ring):
+    """(3,3,3) naive 27, 2051 walkers, 1500 steps in three launches; 32 sampled
+    trajectories bit-exact."""
+    W, steps, seed = 2051, 1500, WORKLOADS["c2_333_zt"].seed + 7
+    g = _ctx(fg, kernel, 3, 3, 3, ring, 32, W)
+    g.seed_naive()
+    p = fg.params_default(phase_steps=500)
+    g.walk(steps, seed, p)
+    got = g.get_walkers()
+    ids = sample_walkers(W, 32, seed=3 + ring)
+    ref = orc.run_walkers(3, 3, 3, ring, 32, 0, 0, steps, seed, ids=ids)
+    _check(got, ref, ids)
+    assert g.stats()["verify_fail"] == 0
+
+
+@pytest.mark.parametrize("kernel", ["t1", "q4"])
+def test_kernel_small_rcap_and_edge(fg, orc, kernel):
+    """R < 32 (expand hits the row cap) and a format with 1-element factors."""
+    for (m, n, p, R, steps) in [((2), 2, 2, 9, 6000), (1, 2, 3, 8, 4000), (2, 3, 2, 14, 5000)]:
+        W, seed = 37, 0x5EED + R
+        g = _ctx(fg, kernel, m, n, p, ZT, R, W)
+        g.seed_naive()
+        g.walk(steps, seed)
+        got = g.get_walkers()
+        ref = orc.run_walkers(m, n, p, ZT, R, W, 0, steps, seed)
+        _check(got, ref, None)
