@@ -94,6 +94,6 @@ cudaError_t fg_launch_restart(uint64_t *cur, uint64_t *best, fg_whdr *hdr, int64
 int fg_kind_for_mode(int kind);
 cudaError_t fg_launch_verify_flagged(const uint64_t *best, fg_whdr *hdr, int64_t num_walkers, int R, int m,
                                      int n, int p, int ring, uint32_t *fail_count, unsigned long long *done,
-                                     cudaStream_t st);   // R24 runs on the one-walker-per-warp / multi-row kernels
+                                     cudaStream_t st);   // R24 runs on the quad, one-walker-per-warp and multi-row kernels
 cudaError_t fg_launch_bestkey(const uint64_t *best, const fg_whdr *hdr, int64_t num_walkers, int R, int mp,
                               unsigned long long *key, cudaStream_t st);

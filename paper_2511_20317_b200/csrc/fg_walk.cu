@@ -603,12 +603,10 @@ int fg_kind_for_mode(int kind)
 {
     switch (kind) {
     case FG_K_H16_P16:
-    case FG_K_T1_P16:
-    case FG_K_Q4_P16: return FG_K_W32_ZT_K16;
+    case FG_K_T1_P16: return FG_K_W32_ZT_K16;
     case FG_K_H16_P32: return FG_K_W32_ZT_K32;
     case FG_K_H16_Z2:
-    case FG_K_T1_Z2:
-    case FG_K_Q4_Z2: return FG_K_W32_Z2_K32;
+    case FG_K_T1_Z2: return FG_K_W32_Z2_K32;
     default: return kind;
     }
 }

@@ -50,7 +50,7 @@ __device__ __forceinline__ int nth_bit_q4(uint32_t x, uint32_t t)
     return __ffs(x) - 1;
 }
 
-template <class P>
+template <class P, bool CM>
 __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
 {
     typedef typename P::F F;
@@ -554,6 +554,8 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
             bool v = searching && att < kf;
             const F ny = P::add(fac(al, Y), sneg ? P::neg(yb) : yb, v);   // y_a + s y_b
             const F nz = P::sub(fac(be, Z), fac(al, Z), v);             // z_b - z_a
+            // R24: no reduction edges -> a draw making a factor zero is rejected
+            if (CM) v = v && !P::zero(ny) && !P::zero(nz);
             const uint32_t bal = (__ballot_sync(FULL, v) >> qb) & 15u;
             const int src = bal ? __ffs(bal) - 1 : 0;
             const uint32_t info = __shfl_sync(FULL, (uint32_t)(al | (be << 8) | (Y << 16) | (Z << 18)), qb | src);
@@ -577,7 +579,27 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         commit_factor(ok, alpha, e_Y, e_ny);
         commit_factor(ok, beta, e_Z, e_nz);
 
-        if (!ok) {
+        if (CM) {
+            // ---- R24 step: flips only; best by (rank, naive additions) ----
+            if (ok) {
+                c_flips++;
+                flags |= 1u;
+                const int adds = nnz_cur - 2 * r - a.mp;
+                const bool better = r < best || (r == best && adds < best_adds);
+                if (better || (r == best && adds == best_adds && (bern & 1u))) {
+                    best = r;
+                    best_adds = adds;
+                    c_copy++;
+                    flags |= 4u;
+                    copy_best();
+                    if (better) {
+                        flags |= 8u;
+                        c_impr++;
+                        enqueue_verify();
+                    }
+                }
+            }
+        } else if (!ok) {
             // expand; continue
             const bool ex = expand();
             c_eok += ex;
@@ -621,8 +643,8 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
             }
         }
         // ---- digest ----
-        const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)best << 10) | ((uint64_t)flags << 20) |
-                            ((uint64_t)alpha << 32) | ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
+        const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)(CM ? (best_adds & 1023) : best) << 10) |
+                            ((uint64_t)flags << 20) | ((uint64_t)alpha << 32) | ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
         digest = (digest ^ ev) * 0x100000001b3ULL;
         digest ^= digest >> 32;
     }
@@ -681,7 +703,10 @@ cudaError_t launch_q4(const WalkArgs &a, cudaStream_t st)
 {
     const int64_t per_block = Q4_WARPS * 8;
     const int64_t blocks = (a.num_walkers + per_block - 1) / per_block;
-    walk_q4<P><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(a);
+    if (a.mode == 1)
+        walk_q4<P, true><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(a);
+    else
+        walk_q4<P, false><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(a);
     return cudaGetLastError();
 }
 
