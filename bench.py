@@ -42,6 +42,12 @@ def parse():
 
 
 # ---------------- integer roofline ----------------
+# (kernel, workload) -> (dram bytes per launch, profile it comes from)
+NCU_TRAFFIC = {
+    ("walk_q4<P16>", "c2_333_zt"): (52.571648e6 + 4.700160e6, "profiles/r01_ncu_walk_q4.txt"),
+}
+
+
 def model_ops_per_step(ring: int, r: float) -> float:
     """SURVEY.md 8(d) per-step algorithmic int32 ops: Z_T 30 r + 200, Z_2 15 r + 180."""
     return 30.0 * r + 200.0 if ring == 0 else 15.0 * r + 180.0
@@ -233,8 +239,12 @@ def main():
     achieved = ops / (per_launch_ms / 1000.0) / 1e12
     sm_mhz = clk.get("sm_mhz") or 1965.0
     peak = int_peak_tops(sm_mhz)
+    # DRAM bytes per launch from the committed `ncu --set full` capture of this kernel
+    # on this workload (dram__bytes_read.sum + dram__bytes_write.sum), if there is one
+    traffic = NCU_TRAFFIC.get((g.kernel_name, args.workload))
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": traffic[0] if traffic else None,
+                "traffic_unit": "B/launch", "traffic_source": traffic[1] if traffic else None,
                 "kernel": g.kernel_name, "kernel_ms_per_launch": per_launch_ms,
                 "kernel_share_of_step": walk_ms / total_ms if total_ms else None,
                 "ops_per_step_model": model_ops_per_step(wl.ring, r_mean),
