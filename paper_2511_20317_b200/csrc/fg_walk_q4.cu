@@ -34,10 +34,10 @@
 
 using namespace fgd;
 
-#define Q4_THREADS 128
+#define Q4_THREADS 32
 #define Q4_WARPS (Q4_THREADS / 32)
 #ifndef Q4_MINB
-#define Q4_MINB 4
+#define Q4_MINB 16
 #endif
 
 namespace {
@@ -234,19 +234,77 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         if (fresh || k2 != o2) set_class(std::false_type{}, l, 2, k2, fresh, true);
         wneg = (wneg & ~(1u << l)) | ((uint32_t)P::first_neg(x.w) << l);
     };
-    // factor Y of row l becomes val (actual sign) if `act`; the row's other factors
-    // are normalised, so only this factor can trigger PAPER:429 (R6).  Whole-warp
-    // collective (called by every quad on the main path).
-    auto commit_factor = [&](bool act, int l, int Y, F val) {
-        const F old = FK(l, Y);
-        const bool fn = P::first_neg(val);
-        const F key = (Y == 2 || !fn) ? (Y == 2 ? P::abs(val) : val) : P::neg(val);
+    // the flip commit (A4/A5): factor Y of row la becomes va and factor Z of row lb
+    // becomes vb (actual signs), if `act`.  The rows' other factors are normalised, so
+    // only the new factor can trigger PAPER:429 (R6).  The two class updates touch
+    // different roles (Y != Z), so they commute and run fused: one pass over the owned
+    // rows compares both keys.  Whole-warp collective (every quad calls it).
+    auto commit_pair = [&](bool act, int la, int Y, F va, int lb, int Z, F vb) {
+        const F olda = FK(la, Y), oldb = FK(lb, Z);
+        const bool fna = P::first_neg(va), fnb = P::first_neg(vb);
+        const F ka = Y == 2 ? P::abs(va) : (fna ? P::neg(va) : va);
+        const F kb = Z == 2 ? P::abs(vb) : (fnb ? P::neg(vb) : vb);
         if (act) {
-            nnz_cur += P::popd(val) - P::popd(old);
-            if (Y == 2) wneg = (wneg & ~(1u << l)) | ((uint32_t)fn << l);
-            else wneg ^= (uint32_t)fn << l;
+            nnz_cur += P::popd(va) - P::popd(olda) + P::popd(vb) - P::popd(oldb);
+            if (Y == 2) wneg = (wneg & ~(1u << la)) | ((uint32_t)fna << la);
+            else wneg ^= (uint32_t)fna << la;
+            if (Z == 2) wneg = (wneg & ~(1u << lb)) | ((uint32_t)fnb << lb);
+            else wneg ^= (uint32_t)fnb << lb;
         }
-        set_class(std::true_type{}, l, Y, key, false, act && key != old);
+        const bool acta = act && ka != olda, actb = act && kb != oldb;
+        const uint32_t ba = 1u << la, bb = 1u << lb;
+        const uint32_t moa = acta ? (MK(la, Y) & ~ba) : 0u;
+        const uint32_t mob = actb ? (MK(lb, Z) & ~bb) : 0u;
+        __syncwarp();                              // old state read by all
+        if (acta && owner(la)) FK(la, Y) = ka;
+        if (actb && owner(lb)) FK(lb, Z) = kb;
+        uint32_t mna = 0, mnb = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int j = 4 * k + q;
+            mna |= (FK(j, Y) == ka) ? (1u << j) : 0u;
+            mnb |= (FK(j, Z) == kb) ? (1u << j) : 0u;
+        }
+        mna |= __shfl_xor_sync(FULL, mna, 1);
+        mnb |= __shfl_xor_sync(FULL, mnb, 1);
+        mna |= __shfl_xor_sync(FULL, mna, 2);
+        mnb |= __shfl_xor_sync(FULL, mnb, 2);
+        const uint32_t live = live_mask();
+        mna = acta ? (mna & live & ~ba) : 0u;
+        mnb = actb ? (mnb & live & ~bb) : 0u;
+        const uint32_t onea = 1u << (10 * Y), oneb = 1u << (10 * Z);
+        for (uint32_t t = (moa | mna) & own; t; t &= t - 1u) {
+            const int m = __ffs(t) - 1;
+            const bool was = (moa >> m) & 1u;
+            const uint32_t mk = MK(m, Y);
+            MK(m, Y) = was ? (mk & ~ba) : (mk | ba);
+            if (m < la) LK(m) += was ? (0u - onea) : onea;
+        }
+        for (uint32_t t = (mob | mnb) & own; t; t &= t - 1u) {
+            const int m = __ffs(t) - 1;
+            const bool was = (mob >> m) & 1u;
+            const uint32_t mk = MK(m, Z);
+            MK(m, Z) = was ? (mk & ~bb) : (mk | bb);
+            if (m < lb) LK(m) += was ? (0u - oneb) : oneb;
+        }
+        if (acta) {
+            const uint32_t ab = above_of(la);
+            if (owner(la)) {
+                MK(la, Y) = mna | ba;
+                LK(la) += (uint32_t)(__popc(mna & ab) - __popc(moa & ab)) << (10 * Y);
+            }
+            nCp += (uint32_t)(__popc(mna) - __popc(moa)) << (10 * Y);
+        }
+        if (actb) {
+            const uint32_t ab = above_of(lb);
+            if (owner(lb)) {
+                MK(lb, Z) = mnb | bb;
+                LK(lb) += (uint32_t)(__popc(mnb & ab) - __popc(mob & ab)) << (10 * Z);
+            }
+            nCp += (uint32_t)(__popc(mnb) - __popc(mob)) << (10 * Z);
+        }
+        pdirty = pdirty || acta || actb;
+        __syncwarp();
     };
     auto unlink = [&](int l, int X) {
         const uint32_t bl = 1u << l;
@@ -576,8 +634,7 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         if (nC && !ok) draws = kf;
         c_draws += draws;
         // commit the flip (every quad takes part; `ok` gates the update)
-        commit_factor(ok, alpha, e_Y, e_ny);
-        commit_factor(ok, beta, e_Z, e_nz);
+        commit_pair(ok, alpha, e_Y, e_ny, beta, e_Z, e_nz);
 
         if (CM) {
             // ---- R24 step: flips only; best by (rank, naive additions) ----
