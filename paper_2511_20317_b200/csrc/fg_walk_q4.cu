@@ -44,9 +44,14 @@ namespace {
 
 enum : int { SF = 0, SMK = 96, SL = 192, SP = 224, SB = 256, Q4_SLOTS = 352 };
 
+// position of the t-th (0-based) set bit of x; t is almost always 0..2 (flip classes
+// are small): predicated clears, a loop only beyond
 __device__ __forceinline__ int nth_bit_q4(uint32_t x, uint32_t t)
 {
-    for (uint32_t k = 0; k < t; ++k) x &= x - 1u;
+    x = t > 0 ? (x & (x - 1u)) : x;
+    x = t > 1 ? (x & (x - 1u)) : x;
+    x = t > 2 ? (x & (x - 1u)) : x;
+    for (uint32_t k = 3; k < t; ++k) x &= x - 1u;
     return __ffs(x) - 1;
 }
 
@@ -534,7 +539,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
 #pragma unroll 1
     for (uint32_t it = 0; it < nsteps; ++it, ++step) {
-        __syncwarp();
         // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1-3 block 2 (draws 1-4)
         uint32_t cb = q == 0 ? 0u : 2u;
         uint32_t c0, c1, c2, c3;

@@ -10,7 +10,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIBFG = os.path.join(HERE, "libfg.so")
+LIBFG = os.environ.get("FG_LIBFG") or os.path.join(HERE, "libfg.so")   # override: A/B experiments only
 
 FG_ZT, FG_Z2 = 0, 1
 FG_FLAG_COMPLEXITY = 1
