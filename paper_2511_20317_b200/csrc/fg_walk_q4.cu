@@ -372,76 +372,75 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     uint32_t c_draws = 0, c_flips = 0, c_red = 0, c_eok = 0, c_erej = 0, c_merge = 0, c_zero = 0,
              c_copy = 0, c_impr = 0;
 
-    // R12: exact worklist reduction after a flip touching rows a0, b0
-    auto slow_local_reduce = [&](int a0, int b0) {
-        int wl0 = a0, wl1 = b0, nwl = 2;
-        while (nwl > 0) {
-            const int t = wl0;
-            wl0 = wl1;
-            nwl--;
-            if (t >= r) continue;
-            if (row_zero(t)) {
-                remove_row(t, wl0, wl1, nwl);
-                c_zero++;
-                continue;
-            }
-            const Row<P> rt = read_row(t);
+    // R12 (local: worklist {a0, b0}) and R15 (global: lexicographic scan) reductions,
+    // exact.  One action per iteration -- a zero-row removal or a merge (write the merged
+    // row, remove the other, remove the merged one too if it has a zero factor) -- so
+    // the class-updating code is inlined once.  Collective over the quad.
+    auto reduce_rows = [&](bool local, int a0, int b0) {
+        int wl0 = a0, wl1 = b0, nwl = local ? 2 : 0;
+        for (;;) {
+            int rm0 = -1, rm1 = -1, wr = -1, lo = -1;
+            bool push = false;
             Row<P> merged;
-            int j = -1;
-            for (uint32_t c = two_of(t) & live_mask(); c; c &= c - 1u) {
-                const int jj = __ffs(c) - 1;
-                if (reducible<P>(rt, read_row(jj), merged)) { j = jj; break; }
-            }
-            if (j < 0) continue;
-            const int lo = t < j ? t : j, hi = t < j ? j : t;
-            write_row(lo, merged, false);
-            c_merge++;
-            remove_row(hi, wl0, wl1, nwl);
-            if (has_zero(merged)) {
-                remove_row(lo, wl0, wl1, nwl);
-                c_zero++;
+            merged.u = merged.v = merged.w = 0;
+            if (local) {
+                if (nwl == 0) break;
+                const int t = wl0;
+                wl0 = wl1;
+                nwl--;
+                if (t >= r) continue;
+                if (row_zero(t)) {
+                    rm0 = t;
+                    c_zero++;
+                } else {
+                    const Row<P> rt = read_row(t);
+                    int j = -1;
+                    for (uint32_t c = two_of(t) & live_mask(); c; c &= c - 1u) {
+                        const int jj = __ffs(c) - 1;
+                        if (reducible<P>(rt, read_row(jj), merged)) { j = jj; break; }
+                    }
+                    if (j < 0) continue;
+                    lo = t < j ? t : j;
+                    wr = lo;
+                    rm0 = t < j ? j : t;
+                    c_merge++;
+                    if (has_zero(merged)) { rm1 = lo; c_zero++; } else push = true;
+                }
             } else {
+                for (int l = 0; l < r; ++l)
+                    if (row_zero(l)) { rm0 = l; break; }
+                if (rm0 >= 0) {
+                    c_zero++;
+                } else {
+                    for (int i = 0; i < r && wr < 0; ++i) {
+                        const uint32_t c0 = two_of(i) & above_of(i) & live_mask();
+                        if (!c0) continue;
+                        const Row<P> ri = read_row(i);
+                        for (uint32_t c = c0; c; c &= c - 1u) {
+                            const int j = __ffs(c) - 1;
+                            if (!reducible<P>(ri, read_row(j), merged)) continue;
+                            wr = i;
+                            rm0 = j;
+                            break;
+                        }
+                    }
+                    if (wr < 0) break;
+                    c_merge++;
+                    if (has_zero(merged)) { rm1 = wr; c_zero++; }
+                }
+            }
+            if (wr >= 0) write_row(wr, merged, false);
+#pragma unroll 1
+            for (int k = 0; k < 2; ++k) {
+                const int h = k == 0 ? rm0 : rm1;
+                if (h < 0) break;
+                remove_row(h, wl0, wl1, nwl);
+            }
+            if (push) {
                 wl1 = wl0;
                 wl0 = lo;
                 nwl++;
             }
-        }
-    };
-
-    // R15 reduce_all, exact
-    auto slow_reduce_all = [&]() {
-        for (;;) {
-            int z = -1;
-            for (int l = 0; l < r; ++l)
-                if (row_zero(l)) { z = l; break; }
-            if (z >= 0) {
-                int n0 = 0, x0 = 0, x1 = 0;
-                remove_row(z, x0, x1, n0);
-                c_zero++;
-                continue;
-            }
-            bool merged_any = false;
-            for (int i = 0; i < r && !merged_any; ++i) {
-                const uint32_t c0 = two_of(i) & above_of(i) & live_mask();
-                if (!c0) continue;
-                const Row<P> ri = read_row(i);
-                for (uint32_t c = c0; c; c &= c - 1u) {
-                    const int j = __ffs(c) - 1;
-                    Row<P> merged;
-                    if (!reducible<P>(ri, read_row(j), merged)) continue;
-                    write_row(i, merged, false);
-                    c_merge++;
-                    int n0 = 0, x0 = 0, x1 = 0;
-                    remove_row(j, x0, x1, n0);
-                    if (has_zero(merged)) {
-                        remove_row(i, x0, x1, n0);
-                        c_zero++;
-                    }
-                    merged_any = true;
-                    break;
-                }
-            }
-            if (!merged_any) break;
         }
     };
 
@@ -671,7 +670,7 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
             c_flips++;
             flags |= 1u;
             // ---- R12 local reduction (exact skip through the masks) ----
-            if (P::zero(e_ny) || P::zero(e_nz) || two_of(alpha) || two_of(beta)) slow_local_reduce(alpha, beta);
+            if (P::zero(e_ny) || P::zero(e_nz) || two_of(alpha) || two_of(beta)) reduce_rows(true, alpha, beta);
             // ---- PAPER:310-313 acceptance ----
             const bool strict = r < best;
             if (strict || (r == best && (bern & 1u))) {
@@ -691,7 +690,7 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
                 c_red++;
                 flags |= 16u;
                 if (maybe) {
-                    slow_reduce_all();
+                    reduce_rows(false, 0, 0);
                     maybe = false;
                 }
             }
