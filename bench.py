@@ -44,7 +44,7 @@ def parse():
 # ---------------- integer roofline ----------------
 # (kernel, workload) -> (dram bytes per launch, profile it comes from)
 NCU_TRAFFIC = {
-    ("walk_q4<P16>", "c2_333_zt"): (52.571648e6 + 4.700160e6, "profiles/r01_ncu_walk_q4.txt"),
+    ("walk_q4<P16>", "c2_333_zt"): (52.543744e6 + 5.945856e6, "profiles/r01_ncu_walk_q4.txt"),
 }
 
 
