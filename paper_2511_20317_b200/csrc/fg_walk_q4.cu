@@ -538,8 +538,9 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
 #pragma unroll 1
     for (uint32_t it = 0; it < nsteps; ++it, ++step) {
-        // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1-3 block 2 (draws 1-4)
-        uint32_t cb = q == 0 ? 0u : 2u;
+        // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1 and 3 block 2
+        // (draws 1-4), lane 2 block 3 (draws 5-8): rounds 0 and 1 need no further block
+        uint32_t cb = q == 0 ? 0u : (q == 2 ? 3u : 2u);
         uint32_t c0, c1, c2, c3;
         philox_block(seed, step, wid, cb, c0, c1, c2, c3);
         const uint32_t bern = __shfl_sync(FULL, (c1 < a.thr_eq ? 1u : 0u) | (c2 < a.thr_reduce ? 2u : 0u) |
@@ -578,7 +579,13 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
             const uint32_t att = 4u * t + (uint32_t)q;
             uint32_t x;
             if (t == 0) {
-                x = q <= 1 ? c0 : (q == 2 ? c1 : c2);
+                const uint32_t s1 = __shfl_sync(FULL, c1, qb | 1);      // block 2 word 1
+                x = q <= 1 ? c0 : (q == 2 ? s1 : c2);
+            } else if (t == 1) {
+                const uint32_t s3 = __shfl_sync(FULL, c3, qb | 1);      // block 2 word 3 (draw 4)
+                const uint32_t u0 = __shfl_sync(FULL, c0, qb | 2);      // block 3 word 0 (draw 5)
+                const uint32_t u2 = __shfl_sync(FULL, c2, qb | 2);      // block 3 word 2 (draw 7)
+                x = q == 0 ? s3 : (q == 1 ? u0 : (q == 2 ? c1 : u2));
             } else {
                 const uint32_t slot = 7u + att, blk = slot >> 2;
                 if (blk != cb) {
