@@ -604,12 +604,12 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
             const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
             const int sh = 10 * X;
             const uint32_t fm = 1023u << sh, qs = qq << sh;
-            int i = 0;
-#pragma unroll
-            for (int st = 16; st >= 1; st >>= 1) {
-                const uint32_t v = PK(i + st) & fm;
-                i += (v <= qs) ? st : 0;
-            }
+            // i = the last row with PF_X(i) <= qq (PF is nondecreasing, PF(0) = 0): three
+            // levels of independent loads (rows 8/16/24, then +2/+4/+6, then +1) instead of
+            // a five-deep dependent binary search
+            int i = 8 * (int)(((PK(8) & fm) <= qs) + ((PK(16) & fm) <= qs) + ((PK(24) & fm) <= qs));
+            i += 2 * (int)(((PK(i + 2) & fm) <= qs) + ((PK(i + 4) & fm) <= qs) + ((PK(i + 6) & fm) <= qs));
+            i += (PK(i + 1) & fm) <= qs ? 1 : 0;
             const uint32_t ex_i = (PK(i) >> sh) & 1023u;
             const uint32_t mm = MK(i, X) & above_of(i);
             const int j = nth_bit_q4(mm, qq - ex_i) & 31;     // (& 31: quads not searching)
