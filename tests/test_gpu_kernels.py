@@ -10,7 +10,7 @@ import os
 import numpy as np
 import pytest
 
-from oracle import Oracle
+from oracle import Oracle, OracleParams
 from paper_2511_20317_b200.inputs import WORKLOADS, sample_walkers
 
 pytestmark = pytest.mark.gpu
@@ -96,3 +96,21 @@ def test_kernel_small_rcap_and_edge(fg, orc, kernel):
         got = g.get_walkers()
         ref = orc.run_walkers(m, n, p, ZT, R, W, 0, steps, seed)
         _check(got, ref, None)
+
+
+@pytest.mark.parametrize("kernel", ["w32", "t1", "q4"])
+def test_kernel_k_flip_round_boundaries(fg, orc, kernel):
+    """K (draws per try_flip, R11) below, at and across the quad kernel's 4-draw rounds,
+    with a high expand rate so flip failures and expands are frequent."""
+    for kf in (1, 3, 5, 7):
+        W, steps, seed = 203, 800, 0xF11 + kf
+        p = fg.params_default(k_flip=kf, thr_expand=1 << 29, expand_slack=3)
+        g = _ctx(fg, kernel, 3, 3, 3, ZT, 32, W)
+        g.seed_naive()
+        g.walk(steps, seed, p)
+        got = g.get_walkers()
+        ids = sample_walkers(W, 12, seed=kf)
+        op = OracleParams.default(k_flip=kf, thr_accept_eq=p.thr_accept_eq, thr_reduce=p.thr_reduce,
+                                  thr_expand=p.thr_expand, expand_slack=p.expand_slack)
+        ref = orc.run_walkers(3, 3, 3, ZT, 32, 0, 0, steps, seed, params=op, ids=ids)
+        _check(got, ref, ids)
