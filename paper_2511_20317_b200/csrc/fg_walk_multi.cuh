@@ -46,7 +46,12 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
         if (lane == 0) v = atomicAdd(a.work_counter, 1ull);
         return (int64_t)__shfl_sync(FULL, v, 0);
     };
-    auto ph = [](int l) { return (l % NS) * 32 + l / NS; };
+    // physical slot of row l, (l % NS) * 32 + l / NS, from a per-CTA table (a division by
+    // the constant NS costs ~5 instructions on every dynamic row access)
+    unsigned short *phtab = reinterpret_cast<unsigned short *>(rc + 8);
+    for (int t = lane; t < NS * 32; t += 32) phtab[t] = (unsigned short)((t % NS) * 32 + t / NS);
+    __syncwarp();
+    auto ph = [&](int l) { return (int)phtab[l]; };
     auto fat = [&](int X, int l) -> F { return sf[X * PLANE + ph(l)]; };
     auto own = [&](int X, int s) -> F { return sf[X * PLANE + s * 32 + lane]; };
 
@@ -727,7 +732,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
 template <class P, int NS, bool CM>
 cudaError_t launch_wm_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
-    const size_t smem = 3 * NS * 32 * sizeof(typename P::F) + 32 * PXS * 4 + 8 * 4;
+    const size_t smem = 3 * NS * 32 * sizeof(typename P::F) + 32 * PXS * 4 + 8 * 4 + NS * 32 * 2;
     int bps = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_wm<P, NS, CM>, 32, smem);
     if (e != cudaSuccess) return e;
