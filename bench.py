@@ -45,8 +45,9 @@ def parse():
 
 # ---------------- integer roofline ----------------
 # (kernel, workload) -> (dram bytes per launch, profile it comes from)
+# and the capture's issue / ALU-pipe utilisation (the north star's "% int-issue" figures)
 NCU_TRAFFIC = {
-    ("walk_q4<P16>", "c2_333_zt"): (52.543744e6 + 5.945856e6, "profiles/r01_ncu_walk_q4.txt"),
+    ("walk_q4<P16>", "c2_333_zt"): (52.543744e6 + 5.945856e6, "profiles/r01_ncu_walk_q4.txt", 57.17, 49.6),
 }
 
 
@@ -248,6 +249,8 @@ def main():
     roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
                 "frac": achieved / peak, "traffic": traffic[0] if traffic else None,
                 "traffic_unit": "B/launch", "traffic_source": traffic[1] if traffic else None,
+                "ncu_issue_active_pct": traffic[2] if traffic else None,
+                "ncu_alu_pipe_pct": traffic[3] if traffic else None,
                 "kernel": g.kernel_name, "kernel_ms_per_launch": per_launch_ms,
                 "kernel_share_of_step": walk_ms / total_ms if total_ms else None,
                 "ops_per_step_model": model_ops_per_step(wl.ring, r_mean),
