@@ -162,7 +162,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         nCp = (uint32_t)qsum((int)part);
         qsync();
     }
-    bool pdirty = true;    // PF stale
     bool maybe = true;     // R15: a full reduce_all may find work
     bool bdirty = false;   // best rows changed in this launch
 
@@ -219,7 +218,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
                 LK(l) += (uint32_t)(__popc(mn & ab) - __popc(mo & ab)) << sh;
             }
             nCp += (uint32_t)(__popc(mn) - __popc(mo)) << sh;
-            pdirty = true;
         }
         __syncwarp(msk);
     };
@@ -308,7 +306,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
             }
             nCp += (uint32_t)(__popc(mnb) - __popc(mob)) << (10 * Z);
         }
-        pdirty = pdirty || acta || actb;
         __syncwarp();
     };
     auto unlink = [&](int l, int X) {
@@ -365,7 +362,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         if (owner(last)) LK(last) = 0;
         wneg &= ~(1u << last);
         r--;
-        pdirty = true;
         qsync();
     };
 
@@ -553,8 +549,9 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         const uint32_t nC = nU + nV + nW;
         int e_Y = 0, e_Z = 0;
         F e_ny = 0, e_nz = 0;
-        // R10 row prefix of the later counts (packed 3 x 10 bits), quad scan per row group
-        if (__any_sync(FULL, nC != 0 && pdirty)) {
+        // R10 row prefix of the later counts (packed 3 x 10 bits), quad scan per row group;
+        // every step (a flip almost always changes a class; a branch on it cost 1 %)
+        {
             uint32_t base = 0;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
@@ -568,7 +565,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
                 PK(4 * k + q) = base + sc - v;
                 base += tot;
             }
-            pdirty = false;
             __syncwarp();
         }
         // R11 try_flip: round t, lane q evaluates draw 4t+q; every quad of the warp
