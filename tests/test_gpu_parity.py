@@ -354,3 +354,26 @@ def test_api_errors_and_stats(fg, orc):
     got = g.get_walkers()
     assert np.all(got["cnt"][:, 0] == 500) and np.all(got["step"] == 500)
     assert int(got["cnt"][:, 2].sum()) == st["flips"]
+
+
+def test_c2_bench_launch_configuration(fg, orc):
+    """The launch configuration bench.py times (C2: 16384 walkers, 10^4-step phases, the
+    default kernel), two phases; 24 sampled trajectories bit-exact, every final and
+    best scheme of a 1-in-16 sample satisfies the Brent equations on the device."""
+    wl = WORKLOADS["c2_333_zt"]
+    W, steps = wl.walkers, 20000
+    g = _ctx(fg, 3, 3, 3, ZT, wl.r_cap, W)
+    g.seed_naive()
+    p = fg.params_default(phase_steps=10000)
+    g.walk(steps, wl.seed, p)
+    got = g.get_walkers()
+    ids = sample_walkers(W, 24, seed=2025)
+    ref = orc.run_walkers(3, 3, 3, ZT, wl.r_cap, 0, 0, steps, wl.seed, ids=ids)
+    _assert_same(got, ref, idx=ids, what="c2-bench")
+    st = g.stats()
+    assert st["verify_fail"] == 0 and st["walk_launches"] == 2
+    sample = list(range(0, W, 16))
+    ok, _ = g.verify_batch([got["rows"][k][: got["r"][k]] for k in sample])
+    assert np.all(ok == 1)
+    ok, _ = g.verify_batch([got["best"][k][: got["best_r"][k]] for k in sample])
+    assert np.all(ok == 1)
