@@ -596,6 +596,12 @@ int fg_pick_kernel(int ring, int maxlen, int R)
         if (h16) return FG_K_H16_Z2;
         return w32 ? FG_K_W32_Z2_K32 : (t1 ? FG_K_T1_Z2 : FG_K_Q4_Z2);
     }
+    // 33 <= R <= 128, one-word factors: the linked-class quad kernel on request
+    const char *env = getenv("FG_WALK_KERNEL");
+    if (R <= 128 && env && strcmp(env, "ql") == 0) {
+        if (ring == FG_ZT && maxlen <= 16) return FG_K_QL_P16;
+        if (ring == FG_Z2 && maxlen <= 32) return FG_K_QL_Z2;
+    }
     return fg_multi_kind(ring, maxlen, R);
 }
 
@@ -607,6 +613,8 @@ int fg_kind_for_mode(int kind)
     case FG_K_H16_P32: return FG_K_W32_ZT_K32;
     case FG_K_H16_Z2:
     case FG_K_T1_Z2: return FG_K_W32_Z2_K32;
+    case FG_K_QL_P16: return FG_K_WM_P16;
+    case FG_K_QL_Z2: return FG_K_WM_Z2;
     default: return kind;
     }
 }
@@ -629,6 +637,8 @@ const char *fg_kernel_kind_name(int kind)
     case FG_K_T1_Z2: return "walk_t1<PZ2>";
     case FG_K_Q4_P16: return "walk_q4<P16>";
     case FG_K_Q4_Z2: return "walk_q4<PZ2>";
+    case FG_K_QL_P16: return "walk_ql<P16>";
+    case FG_K_QL_Z2: return "walk_ql<PZ2>";
     default: return "none";
     }
 }
@@ -646,6 +656,8 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_T1_Z2: return fg_launch_walk_t1(kind, a, st);
     case FG_K_Q4_P16:
     case FG_K_Q4_Z2: return fg_launch_walk_q4(kind, a, st);
+    case FG_K_QL_P16:
+    case FG_K_QL_Z2: return fg_launch_walk_ql(kind, a, st);
     default: return fg_launch_walk_multi(kind, fg_multi_ns(a.R), a, num_sms, st);
     }
 }

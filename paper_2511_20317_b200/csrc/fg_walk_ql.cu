@@ -1,0 +1,770 @@
+// fg_walk_ql.cu -- the RandomWalk kernel (Algorithm 1) for walkers
+// with 33..128 rows and one-word factors (Z_T <= 16 elements, Z_2 <= 32): ONE WALKER
+// PER QUAD, like fg_walk_q4.cu, with the flip classes kept as LINKED LISTS.
+//
+// Why: walk_q4 keeps one class mask per row and role (R bits); at R = 96 that is 3.4 KB
+// per walker and 8 walkers per warp would not fit shared memory.  Here every row keeps,
+// per role, the next and the previous row of its class in row order (bytes), which is
+// all R10/R11 need: the t-th later member of row i is t+1 `next` hops, and the later
+// count of a row (the length of its `next` chain) is kept explicitly.  A class change
+// finds the new class with one compare pass over the rows (split over the quad) and
+// splices the row in; leaving a class relinks the neighbours and walks the `prev`
+// chain to decrement the later counts below.
+//
+// Per walker (shared memory, per warp stride 8 as in walk_q4; lane q owns rows l % 4 == q):
+//   F(l,X)  row l's factor X key (W up to sign, the sign in the register mask wneg)
+//   NX(l)   next row of l's U / V / W class (bytes 0..2, 0xFF = none)
+//   PV(l)   previous row, same packing
+//   L(l)    later counts, 3 x 10 bits
+//   G(g)    later counts before row group g (8 rows): word 0 = U | V << 16, word 1 = W
+// The best scheme lives in HBM (written on acceptance).
+//
+// Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
+// tests/test_gpu_kernels.py.
+#include <type_traits>
+#include "fg_device.cuh"
+
+using namespace fgd;
+
+#define QL_THREADS 32
+
+namespace {
+
+constexpr int NIL = 0xFF;
+
+template <class P, int NWD>
+__global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
+{
+    typedef typename P::F F;
+    static_assert(sizeof(F) == 4, "one-word factor layouts only");
+    constexpr int RM = 32 * NWD;                 // row capacity of this instantiation
+    constexpr int NG = RM / 8;                   // row groups of the prefix
+    constexpr int S_NX = 3 * RM, S_PV = 4 * RM, S_L = 5 * RM, S_G = 6 * RM;
+    constexpr int SLOTS = 6 * RM + 2 * NG;
+    extern __shared__ uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int q = lane & 3;
+    const int qb = lane & 28;
+    const unsigned qm = 0xFu << qb;
+    uint32_t *const S = smem + (threadIdx.x >> 5) * SLOTS * 8 + (lane >> 2);
+    const int64_t wk_raw = ((int64_t)blockIdx.x * (QL_THREADS / 32) + (threadIdx.x >> 5)) * 8 + (lane >> 2);
+    // a quad past the last walker stays in the warp (r = 0, no stores)
+    const bool valid = wk_raw < a.num_walkers;
+    const int64_t wk = valid ? wk_raw : 0;
+
+#define FK(l, X) S[(3 * (l) + (X)) * 8]
+#define NXW(l) S[(S_NX + (l)) * 8]
+#define PVW(l) S[(S_PV + (l)) * 8]
+#define LK(l) S[(S_L + (l)) * 8]
+#define GK(g, h) S[(S_G + 2 * (g) + (h)) * 8]
+
+    auto owner = [&](int l) __attribute__((always_inline)) -> bool { return (l & 3) == q; };
+    auto qsync = [&]() __attribute__((always_inline)) { __syncwarp(qm); };
+    auto byte_of = [](uint32_t w, int X) __attribute__((always_inline)) -> int { return (int)((w >> (8 * X)) & 0xFFu); };
+    auto nxt = [&](int l, int X) __attribute__((always_inline)) -> int { return byte_of(NXW(l), X); };
+    auto prv = [&](int l, int X) __attribute__((always_inline)) -> int { return byte_of(PVW(l), X); };
+    auto set_byte = [](uint32_t w, int X, int v) __attribute__((always_inline)) -> uint32_t {
+        return (w & ~(0xFFu << (8 * X))) | (((uint32_t)v & 0xFFu) << (8 * X));
+    };
+    auto below_in = [](int l, int w) __attribute__((always_inline)) -> uint32_t {      // bits of mask word w for rows < l
+        const int b = l - 32 * w;
+        return b <= 0 ? 0u : (b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u));
+    };
+    auto above_in = [](int l, int w) __attribute__((always_inline)) -> uint32_t {      // bits of mask word w for rows > l
+        const int b = l - 32 * w;
+        return b < 0 ? 0xFFFFFFFFu : (b >= 31 ? 0u : ~((2u << b) - 1u));
+    };
+
+    const int R = a.R;
+    const uint64_t seed = a.seed;
+    const uint32_t kf = a.k_flip;
+    const uint32_t wid = (uint32_t)(a.id_base + wk);
+    fg_whdr *hp = a.hdr + wk;
+    const uint64_t *cp = a.cur + (size_t)wk * FG_PLANES * R;
+    uint64_t *bw = a.best + (size_t)wk * FG_PLANES * R;
+
+    int r = valid ? hp->r : 0;
+    int best = valid ? hp->best_r : 0;
+    uint64_t step = hp->step;
+    uint64_t digest = hp->digest;
+    int best_adds = hp->best_adds;
+
+    // W signs, one bit per row
+    uint32_t wneg[NWD];
+#pragma unroll
+    for (int w = 0; w < NWD; ++w) wneg[w] = 0;
+    auto wbit = [&](int l) __attribute__((always_inline)) -> uint32_t {
+        uint32_t x = 0;
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) x = (l >> 5) == w ? wneg[w] : x;
+        return (x >> (l & 31)) & 1u;
+    };
+    auto set_wbit = [&](int l, uint32_t v) __attribute__((always_inline)) {
+#pragma unroll
+        for (int w = 0; w < NWD; ++w)
+            if ((l >> 5) == w) wneg[w] = (wneg[w] & ~(1u << (l & 31))) | ((v & 1u) << (l & 31));
+    };
+    auto live_in = [&](int w) __attribute__((always_inline)) -> uint32_t { return below_in(r, w); };
+
+    // ---------------- load the walker (own rows) ----------------
+    int nnz_cur = 0;
+#pragma unroll 1
+    for (int l = q; l < RM; l += 4) {
+        F u = 0, v = 0, w = 0;
+        if (l < r) {
+            u = P::make(cp[0 * R + l], cp[1 * R + l]);
+            v = P::make(cp[2 * R + l], cp[3 * R + l]);
+            w = P::make(cp[4 * R + l], cp[5 * R + l]);
+        }
+        nnz_cur += l < r ? P::popd(u) + P::popd(v) + P::popd(w) : 0;
+        set_wbit(l, P::first_neg(w));
+        FK(l, 0) = u; FK(l, 1) = v; FK(l, 2) = P::abs(w);
+    }
+#pragma unroll
+    for (int w = 0; w < NWD; ++w) {
+        wneg[w] |= __shfl_xor_sync(qm, wneg[w], 1);
+        wneg[w] |= __shfl_xor_sync(qm, wneg[w], 2);
+    }
+    nnz_cur += __shfl_xor_sync(qm, nnz_cur, 1);
+    nnz_cur += __shfl_xor_sync(qm, nnz_cur, 2);
+    qsync();
+
+    // class links and later counts from scratch (once per launch): own rows
+    uint32_t nCU = 0, nCV = 0, nCW = 0;     // flip-candidate pairs per role (R10)
+    auto addn = [&](int X, int v) __attribute__((always_inline)) {
+        nCU += X == 0 ? (uint32_t)v : 0u;
+        nCV += X == 1 ? (uint32_t)v : 0u;
+        nCW += X == 2 ? (uint32_t)v : 0u;
+    };
+    {
+        uint32_t pu = 0, pv_ = 0, pw = 0;
+#pragma unroll 1
+        for (int l = q; l < RM; l += 4) {
+            uint32_t nxw = 0xFFFFFFu, pvw = 0xFFFFFFu, lc = 0;
+            if (l < r) {
+#pragma unroll 1
+                for (int X = 0; X < 3; ++X) {
+                    const uint32_t key = FK(l, X);
+                    int nx = NIL, pv = NIL, cnt = 0;
+                    for (int j = 0; j < r; ++j) {
+                        if (j == l || FK(j, X) != key) continue;
+                        if (j < l) pv = j;
+                        else { if (nx == NIL) nx = j; cnt++; }
+                    }
+                    nxw = set_byte(nxw, X, nx);
+                    pvw = set_byte(pvw, X, pv);
+                    lc |= (uint32_t)cnt << (10 * X);
+                }
+            }
+            NXW(l) = nxw; PVW(l) = pvw; LK(l) = lc;
+            pu += lc & 1023u; pv_ += (lc >> 10) & 1023u; pw += lc >> 20;
+        }
+        pu += __shfl_xor_sync(qm, pu, 1); pu += __shfl_xor_sync(qm, pu, 2);
+        pv_ += __shfl_xor_sync(qm, pv_, 1); pv_ += __shfl_xor_sync(qm, pv_, 2);
+        pw += __shfl_xor_sync(qm, pw, 1); pw += __shfl_xor_sync(qm, pw, 2);
+        nCU = pu; nCV = pv_; nCW = pw;
+        qsync();
+    }
+    bool maybe = true;     // R15: a full reduce_all may find work
+
+    auto fac = [&](int l, int X) __attribute__((always_inline)) -> F {
+        const F k = FK(l, X);
+        return (X == 2 && wbit(l)) ? P::neg(k) : k;
+    };
+    auto read_row = [&](int l) __attribute__((always_inline)) -> Row<P> {
+        Row<P> x;
+        x.u = FK(l, 0);
+        x.v = FK(l, 1);
+        const F k = FK(l, 2);
+        x.w = wbit(l) ? P::neg(k) : k;
+        return x;
+    };
+    auto row_zero = [&](int l) __attribute__((always_inline)) -> bool { return P::zero(FK(l, 0)) || P::zero(FK(l, 1)) || P::zero(FK(l, 2)); };
+
+    // ---- class structure primitives ----
+    // leave row l's X class: neighbours relinked, the rows below l lose a later member.
+    // Writes by owners; the caller syncs before the next cross-lane read.
+    auto unlink_role = [&](int l, int X) __attribute__((always_inline)) {
+        const int p = prv(l, X), n = nxt(l, X);
+        const uint32_t lx = (LK(l) >> (10 * X)) & 1023u;
+        int below = 0;
+        for (int m = p; m != NIL; m = prv(m, X)) {
+            if (owner(m)) LK(m) -= 1u << (10 * X);
+            below++;
+        }
+        if (p != NIL && owner(p)) NXW(p) = set_byte(NXW(p), X, n);
+        if (n != NIL && owner(n)) PVW(n) = set_byte(PVW(n), X, p);
+        addn(X, -(below + (int)lx));
+    };
+    // join the class of `key` in role X (FK(l,X) already holds key, written by owner(l)):
+    // one compare pass over the rows, split over the quad.  Collective over msk.
+    auto link_role = [&](auto wtag, int l, int X, uint32_t key, bool act) __attribute__((always_inline)) {
+        constexpr bool WARP = decltype(wtag)::value;
+        const unsigned msk = WARP ? FULL : qm;
+        uint32_t mw[NWD];
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) mw[w] = 0;
+#pragma unroll
+        for (int k = 0; k < RM / 4; ++k) {
+            const int j = 4 * k + q;
+            mw[k >> 3] |= (FK(j, X) == key) ? (1u << (j & 31)) : 0u;
+        }
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) {
+            mw[w] |= __shfl_xor_sync(msk, mw[w], 1);
+            mw[w] |= __shfl_xor_sync(msk, mw[w], 2);
+            mw[w] &= live_in(w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
+        }
+        if (!act) return;
+        int pred = NIL, succ = NIL, nab = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) {
+            const uint32_t lo = mw[w] & below_in(l, w), hi = mw[w] & above_in(l, w);
+            if (lo) pred = 32 * w + 31 - __clz(lo);
+            if (hi && succ == NIL) succ = 32 * w + __ffs(hi) - 1;
+            nab += __popc(hi);
+            tot += __popc(mw[w]);
+        }
+#pragma unroll
+        for (int w = 0; w < NWD; ++w)
+            for (uint32_t t = mw[w] & below_in(l, w) & (0x11111111u << q); t; t &= t - 1u) {
+                const int m = 32 * w + __ffs(t) - 1;
+                LK(m) += 1u << (10 * X);
+            }
+        if (owner(l)) {
+            NXW(l) = set_byte(NXW(l), X, succ);
+            PVW(l) = set_byte(PVW(l), X, pred);
+            LK(l) = (LK(l) & ~(1023u << (10 * X))) | ((uint32_t)nab << (10 * X));
+        }
+        if (pred != NIL && owner(pred)) NXW(pred) = set_byte(NXW(pred), X, l);
+        if (succ != NIL && owner(succ)) PVW(succ) = set_byte(PVW(succ), X, l);
+        addn(X, tot);
+    };
+    // row l's X key becomes `key` (fresh: l is in no X class yet).  Collective over the
+    // quad (wtag false) or the warp (wtag true: every quad calls it, `act` gates it).
+    auto set_class = [&](auto wtag, int l, int X, uint32_t key, bool fresh, bool act) __attribute__((always_inline)) {
+        constexpr bool WARP = decltype(wtag)::value;
+        const unsigned msk = WARP ? FULL : qm;
+        if (act && !fresh) unlink_role(l, X);
+        __syncwarp(msk);
+        if (act && owner(l)) FK(l, X) = key;
+        link_role(wtag, l, X, key, act);
+        __syncwarp(msk);
+    };
+    // store a whole (normalised) row; only changed keys pay a class update.  Quad.
+    auto write_row = [&](int l, const Row<P> &x, bool fresh) __attribute__((always_inline)) {
+        const F o0 = FK(l, 0), o1 = FK(l, 1), o2 = FK(l, 2);
+        if (fresh) {
+            qsync();
+            if (owner(l)) LK(l) = 0;
+        } else {
+            nnz_cur -= P::popd(o0) + P::popd(o1) + P::popd(o2);
+        }
+        nnz_cur += P::popd(x.u) + P::popd(x.v) + P::popd(x.w);
+        const F k0 = x.u, k1 = x.v, k2 = P::abs(x.w);
+        if (fresh || k0 != o0) set_class(std::false_type{}, l, 0, k0, fresh, true);
+        if (fresh || k1 != o1) set_class(std::false_type{}, l, 1, k1, fresh, true);
+        if (fresh || k2 != o2) set_class(std::false_type{}, l, 2, k2, fresh, true);
+        set_wbit(l, P::first_neg(x.w));
+    };
+    // the flip commit: factor Y of row l becomes val (actual sign) if `act`; only this
+    // factor can trigger PAPER:429 (R6).  Whole-warp collective.
+    auto commit_factor = [&](bool act, int l, int Y, F val) __attribute__((always_inline)) {
+        const F old = FK(l, Y);
+        const bool fn = P::first_neg(val);
+        const F key = Y == 2 ? P::abs(val) : (fn ? P::neg(val) : val);
+        if (act) {
+            nnz_cur += P::popd(val) - P::popd(old);
+            if (Y == 2) set_wbit(l, fn);
+            else set_wbit(l, wbit(l) ^ (uint32_t)fn);
+        }
+        set_class(std::true_type{}, l, Y, key, false, act && key != old);
+    };
+    // does a live row other than l share two factors with row l (R13's precondition)?
+    // Such a row is in l's U class (U+V, U+W) or its V class (V+W).
+    auto shares_two = [&](int l) __attribute__((always_inline)) -> bool {
+        const F u = FK(l, 0), v = FK(l, 1), w = FK(l, 2);
+        for (int m = nxt(l, 0); m != NIL; m = nxt(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w) return true;
+        for (int m = prv(l, 0); m != NIL; m = prv(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w) return true;
+        for (int m = nxt(l, 1); m != NIL; m = nxt(m, 1)) if (FK(m, 2) == w) return true;
+        for (int m = prv(l, 1); m != NIL; m = prv(m, 1)) if (FK(m, 2) == w) return true;
+        (void)u;
+        return false;
+    };
+    // rows j (> lmin) sharing two factors with row l, as a row mask
+    auto two_mask = [&](int l, int lmin, uint32_t (&cm)[NWD]) {
+#pragma unroll
+        for (int w = 0; w < NWD; ++w) cm[w] = 0;
+        const F v = FK(l, 1), w_ = FK(l, 2);
+        auto add = [&](int m) __attribute__((always_inline)) {
+            if (m <= lmin) return;
+#pragma unroll
+            for (int w = 0; w < NWD; ++w)
+                if ((m >> 5) == w) cm[w] |= 1u << (m & 31);
+        };
+        for (int m = nxt(l, 0); m != NIL; m = nxt(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w_) add(m);
+        for (int m = prv(l, 0); m != NIL; m = prv(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w_) add(m);
+        for (int m = nxt(l, 1); m != NIL; m = nxt(m, 1)) if (FK(m, 2) == w_) add(m);
+        for (int m = prv(l, 1); m != NIL; m = prv(m, 1)) if (FK(m, 2) == w_) add(m);
+    };
+
+    // R14 remove(h) with the 2-entry worklist (entries == h dropped, r-1 -> h).  Quad.
+    auto remove_row = [&](int h, int &wl0, int &wl1, int &nwl) __attribute__((always_inline)) {
+        const int last = r - 1;
+        int n2 = 0, x0 = 0, x1 = 0;
+        if (nwl >= 1 && wl0 != h) { x0 = wl0; n2 = 1; }
+        if (nwl >= 2 && wl1 != h) { if (n2 == 0) x0 = wl1; else x1 = wl1; n2++; }
+        wl0 = x0; wl1 = x1; nwl = n2;
+        nnz_cur -= P::popd(FK(h, 0)) + P::popd(FK(h, 1)) + P::popd(FK(h, 2));
+        unlink_role(h, 0);
+        qsync();
+        unlink_role(h, 1);
+        qsync();
+        unlink_role(h, 2);
+        qsync();
+        if (h != last) {
+            // row `last` (the largest live index: the tail of each of its classes) moves
+            // to h: in each class it moves down past its members in (h, last), which lose
+            // it as a later member; pred / succ = its new neighbours
+            const F k0 = FK(last, 0), k1 = FK(last, 1), k2 = FK(last, 2);
+            uint32_t nxw = 0xFFFFFFu, pvw = 0xFFFFFFu, lc = 0;
+#pragma unroll 1
+            for (int X = 0; X < 3; ++X) {
+                const int p1 = prv(last, X);
+                int succ = NIL, cnt = 0, m = p1;
+                for (; m != NIL && m > h; m = prv(m, X)) {
+                    if (owner(m)) LK(m) -= 1u << (10 * X);
+                    succ = m;
+                    cnt++;
+                }
+                const int pred = m;
+                qsync();
+                if (p1 != NIL && p1 > h && owner(p1)) NXW(p1) = set_byte(NXW(p1), X, NIL);
+                if (pred != NIL && owner(pred)) NXW(pred) = set_byte(NXW(pred), X, h);
+                if (succ != NIL && owner(succ)) PVW(succ) = set_byte(PVW(succ), X, h);
+                nxw = set_byte(nxw, X, succ);
+                pvw = set_byte(pvw, X, pred);
+                lc |= (uint32_t)cnt << (10 * X);
+                qsync();
+            }
+            if (owner(h)) {
+                FK(h, 0) = k0; FK(h, 1) = k1; FK(h, 2) = k2;
+                NXW(h) = nxw; PVW(h) = pvw; LK(h) = lc;
+            }
+            set_wbit(h, wbit(last));
+            if (nwl >= 1 && wl0 == last) wl0 = h;
+            if (nwl >= 2 && wl1 == last) wl1 = h;
+        }
+        if (owner(last)) LK(last) = 0;
+        set_wbit(last, 0);
+        r--;
+        qsync();
+    };
+
+    uint32_t c_draws = 0, c_flips = 0, c_red = 0, c_eok = 0, c_erej = 0, c_merge = 0, c_zero = 0,
+             c_copy = 0, c_impr = 0;
+
+    // R12 (local: worklist {a0, b0}) and R15 (global: lexicographic scan), exact; one
+    // action per iteration so the merge / removal code is inlined once.  Quad.
+    auto reduce_rows = [&](bool local, int a0, int b0) __attribute__((always_inline)) {
+        int wl0 = a0, wl1 = b0, nwl = local ? 2 : 0;
+        for (;;) {
+            int rm0 = -1, rm1 = -1, wr = -1, lo = -1;
+            bool push = false;
+            Row<P> merged;
+            merged.u = merged.v = merged.w = 0;
+            if (local) {
+                if (nwl == 0) break;
+                const int t = wl0;
+                wl0 = wl1;
+                nwl--;
+                if (t >= r) continue;
+                if (row_zero(t)) {
+                    rm0 = t;
+                    c_zero++;
+                } else {
+                    const Row<P> rt = read_row(t);
+                    uint32_t cm[NWD];
+                    two_mask(t, -1, cm);
+                    int j = -1;
+#pragma unroll
+                    for (int w = 0; w < NWD; ++w)
+                        for (uint32_t c = cm[w]; c && j < 0; c &= c - 1u) {
+                            const int jj = 32 * w + __ffs(c) - 1;
+                            if (reducible<P>(rt, read_row(jj), merged)) j = jj;
+                        }
+                    if (j < 0) continue;
+                    lo = t < j ? t : j;
+                    wr = lo;
+                    rm0 = t < j ? j : t;
+                    c_merge++;
+                    if (has_zero(merged)) { rm1 = lo; c_zero++; } else push = true;
+                }
+            } else {
+                for (int l = 0; l < r; ++l)
+                    if (row_zero(l)) { rm0 = l; break; }
+                if (rm0 >= 0) {
+                    c_zero++;
+                } else {
+                    for (int i = 0; i < r && wr < 0; ++i) {
+                        uint32_t cm[NWD];
+                        two_mask(i, i, cm);
+                        const Row<P> ri = read_row(i);
+#pragma unroll
+                        for (int w = 0; w < NWD; ++w)
+                            for (uint32_t c = cm[w]; c && wr < 0; c &= c - 1u) {
+                                const int j = 32 * w + __ffs(c) - 1;
+                                if (!reducible<P>(ri, read_row(j), merged)) continue;
+                                wr = i;
+                                rm0 = j;
+                            }
+                    }
+                    if (wr < 0) break;
+                    c_merge++;
+                    if (has_zero(merged)) { rm1 = wr; c_zero++; }
+                }
+            }
+            if (wr >= 0) write_row(wr, merged, false);
+#pragma unroll 1
+            for (int k = 0; k < 2; ++k) {
+                const int h = k == 0 ? rm0 : rm1;
+                if (h < 0) break;
+                remove_row(h, wl0, wl1, nwl);
+            }
+            if (push) {
+                wl1 = wl0;
+                wl0 = lo;
+                nwl++;
+            }
+        }
+    };
+
+    // R16 expand (plus / split), words from Philox block 1 of this step.  Quad.
+    auto expand = [&]() __attribute__((always_inline)) -> bool {
+        if (r < 2 || r + 1 > R) return false;
+        uint32_t b0, b1, b2, b3;
+        philox_block(seed, step, wid, 1u, b0, b1, b2, b3);
+        const bool plus = b0 < 0x80000000u;
+        const int i = (int)__umulhi(b1, (uint32_t)r);
+        int j = (int)__umulhi(b2, (uint32_t)(r - 1));
+        j += (j >= i);
+        const int perm = (int)__umulhi(b3, 6u);
+        // PERM = (U,V,W),(U,W,V),(V,U,W),(V,W,U),(W,U,V),(W,V,U)
+        const int A = perm >> 1;
+        const int B = (1161 >> (2 * perm)) & 3;
+        const int Cr = 3 - A - B;
+        Row<P> ri = read_row(i), rj = read_row(j);
+        const F ai = get(ri, A), aj = get(rj, A), bi = get(ri, B), bj = get(rj, B);
+        const F ci = get(ri, Cr), cj = get(rj, Cr);
+        bool ok = true;
+        Row<P> rn;
+        rn.u = rn.v = rn.w = 0;
+        if (plus) {
+            if (!distinct<P>(ai, aj) || !distinct<P>(bi, bj) || !distinct<P>(ci, cj)) return false;
+            const F t1 = P::add(bi, bj, ok);      // v_i + v_j
+            const F t2 = P::sub(cj, ci, ok);      // w_j - w_i
+            const F t3 = P::sub(aj, ai, ok);      // u_j - u_i
+            if (!ok) return false;
+            set(ri, B, t1, true);
+            set(rj, A, ai, true);
+            set(rj, Cr, t2, true);
+            set(rn, A, t3, true);
+            set(rn, B, bj, true);
+            set(rn, Cr, cj, true);
+            normalize<P>(ri);
+            normalize<P>(rj);
+            normalize<P>(rn);
+            write_row(i, ri, false);
+            write_row(j, rj, false);
+        } else {
+            if (!distinct<P>(ai, aj)) return false;
+            const F t3 = P::sub(ai, aj, ok);      // u_i - u_j
+            if (!ok) return false;
+            set(ri, A, aj, true);
+            set(rn, A, t3, true);
+            set(rn, B, bi, true);
+            set(rn, Cr, ci, true);
+            normalize<P>(ri);
+            normalize<P>(rn);
+            write_row(i, ri, false);
+        }
+        r++;
+        write_row(r - 1, rn, true);
+        maybe = true;
+        return true;
+    };
+
+    // store the current rows in plane layout (own rows; zeros above r up to R)
+    auto store_rows = [&](uint64_t *dst) __attribute__((always_inline)) {
+        for (int l = q; l < R; l += 4) {
+            const bool lv = l < r;
+            const F u = lv ? FK(l, 0) : 0, v = lv ? FK(l, 1) : 0, w = lv ? fac(l, 2) : 0;
+            dst[0 * R + l] = P::dig(u); dst[1 * R + l] = P::sgn(u);
+            dst[2 * R + l] = P::dig(v); dst[3 * R + l] = P::sgn(v);
+            dst[4 * R + l] = P::dig(w); dst[5 * R + l] = P::sgn(w);
+        }
+    };
+    // R19 verify queue entry: the current rows (== the new best)
+    auto enqueue_verify = [&]() __attribute__((always_inline)) {
+        unsigned slot = 0;
+        if (q == 0) slot = atomicAdd(a.q_count, 1u);
+        slot = __shfl_sync(qm, slot, qb);
+        if (slot < a.q_cap) {
+            store_rows(a.q_planes + (size_t)slot * FG_PLANES * R);
+            if (q == 0) {
+                fg_qmeta qm_;
+                qm_.walker = wk; qm_.step = step; qm_.rank = r; qm_.ok = -1;
+                qm_.ff[0] = qm_.ff[1] = qm_.ff[2] = -1; qm_.pad = 0;
+                a.q_meta[slot] = qm_;
+            }
+        } else if (q == 0) {
+            atomicAdd(a.q_overflow, 1u);
+            hp->pad |= 1;
+        }
+    };
+
+    const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
+#pragma unroll 1
+    for (uint32_t it = 0; it < nsteps; ++it, ++step) {
+        // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1 and 3 block 2
+        // (draws 1-4), lane 2 block 3 (draws 5-8)
+        uint32_t cb = q == 0 ? 0u : (q == 2 ? 3u : 2u);
+        uint32_t c0, c1, c2, c3;
+        philox_block(seed, step, wid, cb, c0, c1, c2, c3);
+        const uint32_t bern = __shfl_sync(FULL, (c1 < a.thr_eq ? 1u : 0u) | (c2 < a.thr_reduce ? 2u : 0u) |
+                                                    (c3 < a.thr_expand ? 4u : 0u), qb);
+        uint32_t flags = 0;
+        int alpha = 0, beta = 0;
+        uint32_t draws = 0;
+        bool ok = false;
+        const uint32_t nU = nCU, nV = nCV, nW = nCW;
+        const uint32_t nC = nU + nV + nW;
+        int e_Y = 0, e_Z = 0;
+        F e_ny = 0, e_nz = 0;
+        // R10 group prefix of the later counts: lane q sums its two rows of group g
+        {
+            uint32_t bu = 0, bv = 0, bwc = 0;
+#pragma unroll
+            for (int g = 0; g < NG; ++g) {
+                uint32_t s2 = LK(8 * g + q) + LK(8 * g + 4 + q);    // fields <= 2 x 127
+                s2 += __shfl_xor_sync(FULL, s2, 1);
+                s2 += __shfl_xor_sync(FULL, s2, 2);                 // group total, fields <= 1016
+                if (q == (g & 3)) {
+                    GK(g, 0) = bu | (bv << 16);
+                    GK(g, 1) = bwc;
+                }
+                bu += s2 & 1023u;
+                bv += (s2 >> 10) & 1023u;
+                bwc += s2 >> 20;
+            }
+            __syncwarp();
+        }
+        // R11 try_flip: round t, lane q evaluates draw 4t+q (full-warp ballots)
+        bool searching = nC != 0;
+#pragma unroll 1
+        for (uint32_t t = 0; __any_sync(FULL, searching && 4u * t < kf); ++t) {
+            const uint32_t att = 4u * t + (uint32_t)q;
+            uint32_t x;
+            if (t == 0) {
+                const uint32_t s1 = __shfl_sync(FULL, c1, qb | 1);      // block 2 word 1
+                x = q <= 1 ? c0 : (q == 2 ? s1 : c2);
+            } else if (t == 1) {
+                const uint32_t s3 = __shfl_sync(FULL, c3, qb | 1);      // block 2 word 3 (draw 4)
+                const uint32_t u0 = __shfl_sync(FULL, c0, qb | 2);      // block 3 word 0 (draw 5)
+                const uint32_t u2 = __shfl_sync(FULL, c2, qb | 2);      // block 3 word 2 (draw 7)
+                x = q == 0 ? s3 : (q == 1 ? u0 : (q == 2 ? c1 : u2));
+            } else {
+                const uint32_t slot = 7u + att, blk = slot >> 2;
+                if (blk != cb) {
+                    philox_block(seed, step, wid, blk, c0, c1, c2, c3);
+                    cb = blk;
+                }
+                const uint32_t wsel = slot & 3u;
+                x = wsel == 0 ? c0 : (wsel == 1 ? c1 : (wsel == 2 ? c2 : c3));
+            }
+            // ---- R11 draw: k uniform over 4|C| (R9), candidate k>>2 in (X, i, j) order ----
+            const uint32_t k = __umulhi(x, 4u * nC);
+            const uint32_t idx = k >> 2;
+            const int d = k & 1, e = (k >> 1) & 1;
+            const uint32_t g1 = idx >= nU, g2 = idx >= nU + nV;
+            const int X = (int)(g1 + g2);
+            const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
+            // group: the last g with G_X(g) <= qq (G nondecreasing, G(0) = 0)
+            int g = 0;
+#pragma unroll
+            for (int st = 8; st >= 1; st >>= 1) {
+                if (g + st < NG) {
+                    const uint32_t w0 = GK(g + st, 0), w1 = GK(g + st, 1);
+                    const uint32_t v = X == 0 ? (w0 & 0xFFFFu) : (X == 1 ? (w0 >> 16) : w1);
+                    g += v <= qq ? st : 0;
+                }
+            }
+            const uint32_t g0w = GK(g, 0), g1w = GK(g, 1);
+            uint32_t acc = X == 0 ? (g0w & 0xFFFFu) : (X == 1 ? (g0w >> 16) : g1w);
+            // row inside the group: accumulate later counts until past qq
+            int i = 8 * g;
+#pragma unroll 1
+            for (int s = 0; s < 8; ++s) {
+                const uint32_t lx = (LK(8 * g + s) >> (10 * X)) & 1023u;
+                if (acc + lx > qq) { i = 8 * g + s; break; }
+                acc += lx;
+            }
+            // j: the (qq - acc)-th later member of row i's X class
+            int j = i;
+            for (uint32_t hops = qq - acc + 1; hops; --hops) j = nxt(j, X);
+            j = j < RM ? j : 0;                        // (quads not searching: any row)
+            const int al = d ? j : i, be = d ? i : j;
+            // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e
+            const uint32_t yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
+            const int Y = yz & 3, Z = yz >> 2;
+            const bool sneg = P::RING == FG_ZT && X == 2 && (wbit(al) ^ wbit(be));
+            const F yb = fac(be, Y);
+            bool v = searching && att < kf;
+            const F ny = P::add(fac(al, Y), sneg ? P::neg(yb) : yb, v);   // y_a + s y_b
+            const F nz = P::sub(fac(be, Z), fac(al, Z), v);             // z_b - z_a
+            const uint32_t bal = (__ballot_sync(FULL, v) >> qb) & 15u;
+            const int src = bal ? __ffs(bal) - 1 : 0;
+            const uint32_t info = __shfl_sync(FULL, (uint32_t)(al | (be << 8) | (Y << 16) | (Z << 18)), qb | src);
+            const F wny = __shfl_sync(FULL, ny, qb | src);
+            const F wnz = __shfl_sync(FULL, nz, qb | src);
+            if (bal) {
+                alpha = info & 255;
+                beta = (info >> 8) & 255;
+                e_Y = (info >> 16) & 3;
+                e_Z = (info >> 18) & 3;
+                e_ny = wny;
+                e_nz = wnz;
+                draws = 4u * t + (uint32_t)src + 1u;
+                ok = true;
+                searching = false;
+            }
+        }
+        if (nC && !ok) draws = kf;
+        c_draws += draws;
+        // commit the flip (every quad takes part; `ok` gates the update)
+        commit_factor(ok, alpha, e_Y, e_ny);
+        commit_factor(ok, beta, e_Z, e_nz);
+
+        if (!ok) {
+            // expand; continue
+            const bool ex = expand();
+            c_eok += ex;
+            c_erej += !ex;
+            flags |= 2u | (ex ? 64u : 0u);
+            alpha = beta = 0;
+        } else {
+            c_flips++;
+            flags |= 1u;
+            // ---- R12 local reduction (exact skip: zero factor or two shared factors) ----
+            if (P::zero(e_ny) || P::zero(e_nz) || shares_two(alpha) || shares_two(beta))
+                reduce_rows(true, alpha, beta);
+            // ---- PAPER:310-313 acceptance ----
+            const bool strict = r < best;
+            if (strict || (r == best && (bern & 1u))) {
+                best = r;
+                best_adds = nnz_cur - 2 * r - a.mp;
+                c_copy++;
+                flags |= 4u;
+                store_rows(bw);
+                if (strict) {
+                    flags |= 8u;
+                    c_impr++;
+                    enqueue_verify();
+                }
+            }
+            // ---- PAPER:315-317 reduce (R15) ----
+            if (bern & 2u) {
+                c_red++;
+                flags |= 16u;
+                if (maybe) {
+                    reduce_rows(false, 0, 0);
+                    maybe = false;
+                }
+            }
+            // ---- PAPER:319-321 expand ----
+            if ((bern & 4u) && r <= best + a.slack) {
+                const bool ex = expand();
+                flags |= 32u | (ex ? 64u : 0u);
+                c_eok += ex;
+                c_erej += !ex;
+            }
+        }
+        // ---- digest ----
+        const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)best << 10) | ((uint64_t)flags << 20) |
+                            ((uint64_t)alpha << 32) | ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
+        digest = (digest ^ ev) * 0x100000001b3ULL;
+        digest ^= digest >> 32;
+    }
+
+    // ---------------- store own rows; best additions from the best rows in HBM ----------------
+    __syncwarp();
+    if (valid) store_rows(a.cur + (size_t)wk * FG_PLANES * R);
+    int best_nnz = 0;
+    for (int l = q; l < R && valid; l += 4)
+        if (l < best) best_nnz += __popcll(bw[0 * R + l]) + __popcll(bw[2 * R + l]) + __popcll(bw[4 * R + l]);
+    best_nnz += __shfl_xor_sync(qm, best_nnz, 1);
+    best_nnz += __shfl_xor_sync(qm, best_nnz, 2);
+    if (q == 0 && valid) {
+        hp->r = r;
+        hp->best_r = best;
+        hp->step = step;
+        hp->digest = digest;
+        hp->best_adds = best_adds;
+        hp->cnt[FG_CNT_STEPS] += a.steps;
+        hp->cnt[FG_CNT_DRAWS] += c_draws;
+        hp->cnt[FG_CNT_FLIPS] += c_flips;
+        hp->cnt[FG_CNT_FLIP_FAIL] += a.steps - c_flips;
+        hp->cnt[FG_CNT_EXPAND_OK] += c_eok;
+        hp->cnt[FG_CNT_EXPAND_REJECT] += c_erej;
+        hp->cnt[FG_CNT_MERGES] += c_merge;
+        hp->cnt[FG_CNT_ZERO_REMOVED] += c_zero;
+        hp->cnt[FG_CNT_BEST_COPIES] += c_copy;
+        hp->cnt[FG_CNT_IMPROVEMENTS] += c_impr;
+        hp->cnt[FG_CNT_REDUCE_CALLS] += c_red;
+        int adds = best_nnz - 2 * best - a.mp;
+        if (adds < 0) adds = 0;
+        atomicMin(a.best_key, ((unsigned long long)best << 54) | ((unsigned long long)adds << 36) |
+                                  (unsigned long long)wk);
+    }
+#undef FK
+#undef NXW
+#undef PVW
+#undef LK
+#undef GK
+}
+
+template <class P, int NWD>
+cudaError_t launch_ql(const WalkArgs &a, cudaStream_t st)
+{
+    constexpr int RM = 32 * NWD;
+    const size_t smem = (size_t)(6 * RM + 2 * (RM / 8)) * 8 * 4 * (QL_THREADS / 32);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(walk_ql<P, NWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int64_t per_block = (QL_THREADS / 32) * 8;
+    const int64_t blocks = (a.num_walkers + per_block - 1) / per_block;
+    walk_ql<P, NWD><<<(unsigned)blocks, QL_THREADS, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+template <class P>
+cudaError_t launch_ql_r(const WalkArgs &a, cudaStream_t st)
+{
+    if (a.R <= 64) return launch_ql<P, 2>(a, st);
+    if (a.R <= 96) return launch_ql<P, 3>(a, st);
+    return launch_ql<P, 4>(a, st);
+}
+
+}  // namespace
+
+cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, cudaStream_t st)
+{
+    switch (kind) {
+    case FG_K_QL_P16: return launch_ql_r<P16>(a, st);
+    case FG_K_QL_Z2: return launch_ql_r<PZ2>(a, st);
+    default: return cudaErrorInvalidValue;
+    }
+}

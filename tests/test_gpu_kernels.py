@@ -16,6 +16,7 @@ from paper_2511_20317_b200.inputs import WORKLOADS, sample_walkers
 pytestmark = pytest.mark.gpu
 ZT, Z2 = 0, 1
 KERNELS = {"w32": "walk_w32", "h16": "walk_h16", "t1": "walk_t1", "q4": "walk_q4"}
+KERNEL_PREFIX = dict(KERNELS, ql="walk_ql")
 
 
 @pytest.fixture(scope="module")
@@ -43,7 +44,7 @@ def _ctx(fg, kernel, m, n, p, ring, R, W):
             del os.environ["FG_WALK_KERNEL"]
         else:
             os.environ["FG_WALK_KERNEL"] = old
-    assert g.kernel_name.startswith(KERNELS[kernel]), g.kernel_name
+    assert g.kernel_name.startswith(KERNEL_PREFIX[kernel]), g.kernel_name
     return g
 
 
@@ -114,3 +115,22 @@ def test_kernel_k_flip_round_boundaries(fg, orc, kernel):
                                   thr_expand=p.thr_expand, expand_slack=p.expand_slack)
         ref = orc.run_walkers(3, 3, 3, ZT, 32, 0, 0, steps, seed, params=op, ids=ids)
         _check(got, ref, ids)
+
+
+QL_CASES = [((3, 3, 4), ZT, 48, 45, 3000), ((2, 4, 5), Z2, 64, 37, 3000), ((3, 4, 4), ZT, 64, 29, 2500),
+            ((4, 4, 4), ZT, 96, 61, 2000), ((4, 4, 4), Z2, 96, 40, 2000), ((4, 4, 4), ZT, 128, 17, 1500),
+            ((3, 4, 5), Z2, 72, 23, 2000), ((4, 4, 6), Z2, 128, 9, 1000), ((2, 4, 4), ZT, 40, 33, 3000)]
+
+
+@pytest.mark.parametrize("case", QL_CASES, ids=lambda c: f"{c[0]}-{'zt' if c[1] == ZT else 'z2'}-R{c[2]}")
+def test_ql_linked_class_kernel(fg, orc, case):
+    """The linked-class quad kernel (33 <= R <= 128) against the oracle, every walker."""
+    (m, n, p), ring, R, W, steps = case
+    seed = 0x51 + R + ring
+    g = _ctx(fg, "ql", m, n, p, ring, R, W)
+    g.seed_naive()
+    g.walk(steps, seed, fg.params_default(phase_steps=steps // 2 + 1))
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
+    _check(got, ref, None)
+    assert g.stats()["verify_fail"] == 0
