@@ -12,7 +12,7 @@
 // chain to decrement the later counts below.
 //
 // Per walker (shared memory, per warp stride 8 as in walk_q4; lane q owns rows l % 4 == q):
-//   F(l,X)  row l's factor X key (W up to sign, the sign in the register mask wneg)
+//   F(l,X)  row l's factor X key (W up to sign; the sign is bit 24 of NX(l))
 //   NX(l)   next row of l's U / V / W class (bytes 0..2, 0xFF = none)
 //   PV(l)   previous row, same packing
 //   L(l)    later counts, 3 x 10 bits
@@ -89,25 +89,16 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     uint64_t digest = hp->digest;
     int best_adds = hp->best_adds;
 
-    // W signs, one bit per row
-    uint32_t wneg[NWD];
-#pragma unroll
-    for (int w = 0; w < NWD; ++w) wneg[w] = 0;
-    auto wbit = [&](int l) __attribute__((always_inline)) -> uint32_t {
-        uint32_t x = 0;
-#pragma unroll
-        for (int w = 0; w < NWD; ++w) x = (l >> 5) == w ? wneg[w] : x;
-        return (x >> (l & 31)) & 1u;
-    };
-    auto set_wbit = [&](int l, uint32_t v) __attribute__((always_inline)) {
-#pragma unroll
-        for (int w = 0; w < NWD; ++w)
-            if ((l >> 5) == w) wneg[w] = (wneg[w] & ~(1u << (l & 31))) | ((v & 1u) << (l & 31));
+    // W sign of row l: bit 24 of NX(l) (the stored W key is up to sign)
+    auto wbit = [&](int l) __attribute__((always_inline)) -> uint32_t { return (NXW(l) >> 24) & 1u; };
+    auto set_wbit = [&](int l, uint32_t v) __attribute__((always_inline)) {    // owner; caller syncs
+        if (owner(l)) NXW(l) = (NXW(l) & 0x00FFFFFFu) | ((v & 1u) << 24);
     };
     auto live_in = [&](int w) __attribute__((always_inline)) -> uint32_t { return below_in(r, w); };
 
     // ---------------- load the walker (own rows) ----------------
     int nnz_cur = 0;
+    uint32_t own_sign = 0;                       // W signs of own rows (bit l / 4)
 #pragma unroll 1
     for (int l = q; l < RM; l += 4) {
         F u = 0, v = 0, w = 0;
@@ -117,13 +108,8 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             w = P::make(cp[4 * R + l], cp[5 * R + l]);
         }
         nnz_cur += l < r ? P::popd(u) + P::popd(v) + P::popd(w) : 0;
-        set_wbit(l, P::first_neg(w));
+        own_sign |= (uint32_t)P::first_neg(w) << (l >> 2);
         FK(l, 0) = u; FK(l, 1) = v; FK(l, 2) = P::abs(w);
-    }
-#pragma unroll
-    for (int w = 0; w < NWD; ++w) {
-        wneg[w] |= __shfl_xor_sync(qm, wneg[w], 1);
-        wneg[w] |= __shfl_xor_sync(qm, wneg[w], 2);
     }
     nnz_cur += __shfl_xor_sync(qm, nnz_cur, 1);
     nnz_cur += __shfl_xor_sync(qm, nnz_cur, 2);
@@ -156,7 +142,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
                     lc |= (uint32_t)cnt << (10 * X);
                 }
             }
-            NXW(l) = nxw; PVW(l) = pvw; LK(l) = lc;
+            NXW(l) = nxw | (((own_sign >> (l >> 2)) & 1u) << 24); PVW(l) = pvw; LK(l) = lc;
             pu += lc & 1023u; pv_ += (lc >> 10) & 1023u; pw += lc >> 20;
         }
         pu += __shfl_xor_sync(qm, pu, 1); pu += __shfl_xor_sync(qm, pu, 2);
@@ -261,11 +247,15 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             nnz_cur -= P::popd(o0) + P::popd(o1) + P::popd(o2);
         }
         nnz_cur += P::popd(x.u) + P::popd(x.v) + P::popd(x.w);
-        const F k0 = x.u, k1 = x.v, k2 = P::abs(x.w);
-        if (fresh || k0 != o0) set_class(std::false_type{}, l, 0, k0, fresh, true);
-        if (fresh || k1 != o1) set_class(std::false_type{}, l, 1, k1, fresh, true);
-        if (fresh || k2 != o2) set_class(std::false_type{}, l, 2, k2, fresh, true);
+        // one inlined class update, looped over the roles (rare path: code size)
+#pragma unroll 1
+        for (int X = 0; X < 3; ++X) {
+            const F kX = X == 0 ? x.u : (X == 1 ? x.v : P::abs(x.w));
+            const F oX = X == 0 ? o0 : (X == 1 ? o1 : o2);
+            if (fresh || kX != oX) set_class(std::false_type{}, l, X, kX, fresh, true);
+        }
         set_wbit(l, P::first_neg(x.w));
+        qsync();
     };
     // the flip commit: factor Y of row l becomes val (actual sign) if `act`; only this
     // factor can trigger PAPER:429 (R6).  Whole-warp collective.
@@ -275,8 +265,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         const F key = Y == 2 ? P::abs(val) : (fn ? P::neg(val) : val);
         if (act) {
             nnz_cur += P::popd(val) - P::popd(old);
-            if (Y == 2) set_wbit(l, fn);
-            else set_wbit(l, wbit(l) ^ (uint32_t)fn);
+            set_wbit(l, Y == 2 ? (uint32_t)fn : (wbit(l) ^ (uint32_t)fn));
         }
         set_class(std::true_type{}, l, Y, key, false, act && key != old);
     };
@@ -347,16 +336,15 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
                 lc |= (uint32_t)cnt << (10 * X);
                 qsync();
             }
+            const uint32_t sl = wbit(last);
             if (owner(h)) {
                 FK(h, 0) = k0; FK(h, 1) = k1; FK(h, 2) = k2;
-                NXW(h) = nxw; PVW(h) = pvw; LK(h) = lc;
+                NXW(h) = nxw | (sl << 24); PVW(h) = pvw; LK(h) = lc;
             }
-            set_wbit(h, wbit(last));
             if (nwl >= 1 && wl0 == last) wl0 = h;
             if (nwl >= 2 && wl1 == last) wl1 = h;
         }
         if (owner(last)) LK(last) = 0;
-        set_wbit(last, 0);
         r--;
         qsync();
     };
@@ -474,8 +462,6 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             normalize<P>(ri);
             normalize<P>(rj);
             normalize<P>(rn);
-            write_row(i, ri, false);
-            write_row(j, rj, false);
         } else {
             if (!distinct<P>(ai, aj)) return false;
             const F t3 = P::sub(ai, aj, ok);      // u_i - u_j
@@ -486,10 +472,19 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             set(rn, Cr, ci, true);
             normalize<P>(ri);
             normalize<P>(rn);
-            write_row(i, ri, false);
         }
-        r++;
-        write_row(r - 1, rn, true);
+        // rows i, j (plus only) and the new row r; one inlined write_row
+#pragma unroll 1
+        for (int t = 0; t < 3; ++t) {
+            if (t == 1 && !plus) continue;
+            if (t == 2) r++;
+            const int l = t == 0 ? i : (t == 1 ? j : r - 1);
+            Row<P> x;
+            x.u = t == 0 ? ri.u : (t == 1 ? rj.u : rn.u);
+            x.v = t == 0 ? ri.v : (t == 1 ? rj.v : rn.v);
+            x.w = t == 0 ? ri.w : (t == 1 ? rj.w : rn.w);
+            write_row(l, x, t == 2);
+        }
         maybe = true;
         return true;
     };
@@ -655,29 +650,32 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         } else {
             c_flips++;
             flags |= 1u;
-            // ---- R12 local reduction (exact skip: zero factor or two shared factors) ----
-            if (P::zero(e_ny) || P::zero(e_nz) || shares_two(alpha) || shares_two(beta))
-                reduce_rows(true, alpha, beta);
-            // ---- PAPER:310-313 acceptance ----
-            const bool strict = r < best;
-            if (strict || (r == best && (bern & 1u))) {
-                best = r;
-                best_adds = nnz_cur - 2 * r - a.mp;
-                c_copy++;
-                flags |= 4u;
-                store_rows(bw);
-                if (strict) {
-                    flags |= 8u;
-                    c_impr++;
-                    enqueue_verify();
-                }
-            }
-            // ---- PAPER:315-317 reduce (R15) ----
-            if (bern & 2u) {
-                c_red++;
-                flags |= 16u;
-                if (maybe) {
-                    reduce_rows(false, 0, 0);
+            // ---- R12 local reduction (exact skip), PAPER:310-313 acceptance
+            // reduce (R15, exact skip) -- one loop so the reduction code is inlined once ----
+            const bool need_local = P::zero(e_ny) || P::zero(e_nz) || shares_two(alpha) || shares_two(beta);
+#pragma unroll 1
+            for (int ph = 0; ph < 2; ++ph) {
+                const bool run = ph == 0 ? need_local : ((bern & 2u) && maybe);
+                if (run) reduce_rows(ph == 0, alpha, beta);
+                if (ph == 0) {
+                    const bool strict = r < best;
+                    if (strict || (r == best && (bern & 1u))) {
+                        best = r;
+                        best_adds = nnz_cur - 2 * r - a.mp;
+                        c_copy++;
+                        flags |= 4u;
+                        store_rows(bw);
+                        if (strict) {
+                            flags |= 8u;
+                            c_impr++;
+                            enqueue_verify();
+                        }
+                    }
+                    if (bern & 2u) {
+                        c_red++;
+                        flags |= 16u;
+                    }
+                } else if (run) {
                     maybe = false;
                 }
             }
