@@ -47,7 +47,7 @@ def parse():
 # (kernel, workload) -> (dram bytes per launch, profile it comes from)
 # and the capture's issue / ALU-pipe utilisation (the north star's "% int-issue" figures)
 NCU_TRAFFIC = {
-    ("walk_q4<P16>", "c2_333_zt"): (52.543744e6 + 5.945856e6, "profiles/r01_ncu_walk_q4.txt", 57.17, 49.6),
+    ("walk_q4<P16>", "c2_333_zt"): (52.551424e6 + 7.051776e6, "profiles/r01_ncu_walk_q4.txt", 58.89, 50.5),
 }
 
 
