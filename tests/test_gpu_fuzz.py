@@ -31,7 +31,26 @@ def _configs(n=14, seed=20251120):
     return out
 
 
-CONFIGS = _configs()
+def _extreme_configs(n=8, seed=7):
+    """Extreme Alg. 1 parameters: thresholds at 0 / 2^32-1, negative expand slack
+    (PAPER:319 gate never open), K = 1 and 16."""
+    rng = np.random.default_rng(seed)
+    out = []
+    fmts = [(2, 2, 2), (3, 3, 3), (2, 3, 4), (1, 2, 2)]
+    edges = [0, 1, 1 << 31, (1 << 32) - 1]
+    for k in range(n):
+        m, nn, p = fmts[k % len(fmts)]
+        ring = k & 1
+        naive = m * nn * p
+        R = min(32, naive + 1 + k % 5)
+        prm = dict(k_flip=[1, 16][k % 2], thr_accept_eq=int(rng.choice(edges)), thr_reduce=int(rng.choice(edges)),
+                   thr_expand=int(rng.choice(edges)), expand_slack=int(rng.integers(-3, 6)))
+        out.append(((m, nn, p), ring, R, prm, int(rng.integers(9, 70)), int(rng.integers(300, 1500)),
+                    int(rng.integers(1, 1 << 62))))
+    return out
+
+
+CONFIGS = _configs() + _extreme_configs()
 
 
 @pytest.fixture(scope="module")
