@@ -89,3 +89,48 @@ def test_fuzz_config(fg, orc, kernel, idx):
     for k in ("r", "best_r", "digest", "cnt", "rows", "best"):
         assert np.array_equal(got[k], ref[k]), f"config {idx} {CONFIGS[idx]}: {k} differs"
     assert g.stats()["verify_fail"] == 0
+
+
+def _ql_configs(n=8, seed=33):
+    """Formats and row caps for the linked-class quad kernel (33 <= R <= 128, one-word factors)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        m, nn, p = (int(x) for x in rng.integers(2, 5, size=3))
+        ring = int(rng.integers(0, 2))
+        naive = m * nn * p
+        maxlen = max(m * nn, nn * p, p * m)
+        if naive + 2 > 128 or (ring == 0 and maxlen > 16):
+            continue
+        R = int(min(128, max(33, naive + int(rng.integers(2, 12)))))
+        prm = dict(k_flip=int(rng.integers(1, 17)), thr_accept_eq=int(rng.integers(0, 1 << 31)),
+                   thr_reduce=int(rng.integers(0, 1 << 32)), thr_expand=int(rng.integers(0, 1 << 30)),
+                   expand_slack=int(rng.integers(0, 4)))
+        out.append(((m, nn, p), ring, R, prm, int(rng.integers(9, 40)), int(rng.integers(300, 1200)),
+                    int(rng.integers(1, 1 << 62))))
+    return out
+
+
+QL_CONFIGS = _ql_configs()
+
+
+@pytest.mark.parametrize("idx", range(len(QL_CONFIGS)))
+def test_fuzz_ql(fg, orc, idx):
+    import torch
+    (m, n, p), ring, R, prm, W, steps, seed = QL_CONFIGS[idx]
+    old = os.environ.get("FG_WALK_KERNEL")
+    os.environ["FG_WALK_KERNEL"] = "ql"
+    try:
+        g = fg.FlipGraph(m, n, p, ring, R, W, 0, 0, torch.cuda.current_stream().cuda_stream)
+    finally:
+        if old is None:
+            del os.environ["FG_WALK_KERNEL"]
+        else:
+            os.environ["FG_WALK_KERNEL"] = old
+    assert g.kernel_name.startswith("walk_ql"), g.kernel_name
+    g.seed_naive()
+    g.walk(steps, seed, fg.params_default(**prm))
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed, params=OracleParams.default(**prm))
+    for k in ("r", "best_r", "digest", "cnt", "rows", "best"):
+        assert np.array_equal(got[k], ref[k]), f"ql config {idx} {QL_CONFIGS[idx]}: {k} differs"
