@@ -10,7 +10,8 @@
 // step for 2 on average).  A quad is the middle: 4x the warps, and the quad splits
 // the walker's parallel work:
 //   - Philox (R8): lane 0 computes block 0 (draw 0 + the three Bernoulli words),
-//     lanes 1-3 block 2 (draws 1-4) -- one block time per step;
+//     lanes 1 and 3 block 2 (draws 1-4), lane 2 block 3 (draws 5-8) -- one block time
+//     per step covers two draw rounds;
 //   - try_flip (R11): lane q evaluates draw 4t+q in round t; the quad ballot picks the
 //     first valid draw, exactly the draw the sequential loop commits (1.07 rounds per
 //     walker on average instead of 2 draws);
@@ -18,7 +19,9 @@
 //     stores are split by row ownership: lane q owns rows l with l % 4 == q.
 // Every per-walker scalar (r, best, the step, digest, candidate totals, wneg,
 // counters) is replicated in the 4 lanes and evolves identically, so the quad's
-// control flow is uniform and every collective uses the quad mask.
+// control flow is uniform.  The main path (Philox broadcast, row prefix, draw rounds,
+// flip commit) is run by every quad of the warp with full-warp collectives; the rare
+// paths (merges, removals, expand) use quad-mask collectives.
 //
 // Shared memory: per warp a region of T1-style slots with stride 8 (walker w of the
 // warp at word slot*8 + w): a slot access by the 4 lanes of a quad (rows l = q mod 4,
@@ -28,7 +31,7 @@
 // phase from the next cross-lane read.
 //
 // Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
-// tests/test_gpu_parity.py.
+// tests/test_gpu_parity.py, tests/test_gpu_kernels.py, tests/test_gpu_fuzz.py.
 #include <type_traits>
 #include "fg_device.cuh"
 
