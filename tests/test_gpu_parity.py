@@ -377,3 +377,39 @@ def test_c2_bench_launch_configuration(fg, orc):
     assert np.all(ok == 1)
     ok, _ = g.verify_batch([got["best"][k][: got["best_r"][k]] for k in sample])
     assert np.all(ok == 1)
+
+
+def test_virtual_ranks_match_single_gpu(fg):
+    """SURVEY 4.3 multi-GPU: G ranks owning disjoint global walker-id ranges produce,
+    walker by walker, the states of one context over all ids (the trajectory depends
+    only on (seed, global id, step)); the merge of the per-rank best records equals the
+    single context's best.  Two "virtual ranks" on one GPU, with a restart from the
+    merged pool in between (R23), as bench.py's multi-rank path does."""
+    from paper_2511_20317_b200.pool_sync import merge_gathered
+    W, half, steps, seed = 3000, 1500, 2500, 0x2511203170000009
+    one = _ctx(fg, 3, 3, 3, ZT, 32, W, base=0)
+    ranks = [_ctx(fg, 3, 3, 3, ZT, 32, half, base=0), _ctx(fg, 3, 3, 3, ZT, 32, half, base=half)]
+    for g in [one] + ranks:
+        g.seed_naive()
+    for phase in range(2):
+        one.walk(steps, seed + phase)
+        for g in ranks:
+            g.walk(steps, seed + phase)
+        # pool sync: all-gather of the per-rank records, identical merge on every rank
+        recs = np.stack([g.export_best() for g in ranks])
+        merged = merge_gathered(recs, 2, 32)
+        b1 = one.best()
+        assert merged["rank"] == b1["rank"] and merged["walker_id"] == b1["walker_id"]
+        for g in ranks:
+            g.import_best(recs.reshape(-1), 2)
+        one.import_best(np.stack([one.export_best()]).reshape(-1), 1)
+        got1 = one.get_walkers()
+        for k, g in enumerate(ranks):
+            gk = g.get_walkers()
+            sl = slice(k * half, (k + 1) * half)
+            for key in ("r", "best_r", "digest", "cnt", "rows", "best"):
+                assert np.array_equal(gk[key], got1[key][sl]), (phase, k, key)
+        # restart stagnant walkers from the merged pool on every context (same pool)
+        n1 = one.restart(0)
+        nr = sum(g.restart(0) for g in ranks)
+        assert n1 == nr
