@@ -190,7 +190,9 @@ def main():
 
     # time-to-rank ladder: device time since seeding until the box best first <= rank
     ladder = {}
+    ladder_steps = {}            # box walker-steps done when each rank was first reached
     elapsed = [0.0]
+    done_steps = [0]
 
     def phase(timed_events=None):
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -202,8 +204,10 @@ def main():
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1)
         elapsed[0] += ms / 1000.0
+        done_steps[0] += W * S * world
         for target in range(best["rank"], wl.m * wl.n * wl.p):
             ladder.setdefault(target, elapsed[0])
+            ladder_steps.setdefault(target, done_steps[0])
         return ms
 
     for _ in range(args.warmup):
@@ -283,6 +287,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = run_oracle_sample(wl, args.cpu_seconds)
+        # the trajectories are identical on the CPU (parity), so the oracle reaches each
+        # rank after the same walker-steps: time = steps / its measured rate (extrapolated)
+        cpu["time_to_rank_s_extrapolated"] = {str(k): round(v / cpu["value"], 1)
+                                              for k, v in sorted(ladder_steps.items())}
 
     best = g.best()
     stats = {k: st1[k] - st0[k] for k in ("verified", "verify_fail", "queue_overflow")}
