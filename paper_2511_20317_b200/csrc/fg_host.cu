@@ -252,8 +252,6 @@ int seed_planes(fg_ctx *c, const uint64_t *planes, int rank, int64_t w0, int64_t
     CK(cudaStreamSynchronize(c->stream));
     if (rc != FG_OK) return rc;
     c->seeded = true;
-    (void)planes;
-    (void)rank;
     return recompute_local_best(c);
 }
 

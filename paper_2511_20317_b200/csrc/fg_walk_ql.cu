@@ -272,12 +272,11 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     // does a live row other than l share two factors with row l (R13's precondition)?
     // Such a row is in l's U class (U+V, U+W) or its V class (V+W).
     auto shares_two = [&](int l) __attribute__((always_inline)) -> bool {
-        const F u = FK(l, 0), v = FK(l, 1), w = FK(l, 2);
+        const F v = FK(l, 1), w = FK(l, 2);
         for (int m = nxt(l, 0); m != NIL; m = nxt(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w) return true;
         for (int m = prv(l, 0); m != NIL; m = prv(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w) return true;
         for (int m = nxt(l, 1); m != NIL; m = nxt(m, 1)) if (FK(m, 2) == w) return true;
         for (int m = prv(l, 1); m != NIL; m = prv(m, 1)) if (FK(m, 2) == w) return true;
-        (void)u;
         return false;
     };
     // rows j (> lmin) sharing two factors with row l, as a row mask
