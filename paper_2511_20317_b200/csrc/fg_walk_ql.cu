@@ -187,36 +187,33 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     auto link_role = [&](auto wtag, int l, int X, uint32_t key, bool act) __attribute__((always_inline)) {
         constexpr bool WARP = decltype(wtag)::value;
         const unsigned msk = WARP ? FULL : qm;
-        uint32_t mw[NWD];
-#pragma unroll
-        for (int w = 0; w < NWD; ++w) mw[w] = 0;
-#pragma unroll
-        for (int k = 0; k < RM / 4; ++k) {
-            const int j = 4 * k + q;
-            mw[k >> 3] |= (FK(j, X) == key) ? (1u << (j & 31)) : 0u;
-        }
-#pragma unroll
+        // one mask word (32 rows) per iteration, not unrolled: a compact loop body keeps
+        // the instruction stream small (the unrolled 24-row pass missed the i-cache)
+        int pred = NIL, succ = NIL, nab = 0, tot = 0;
+#pragma unroll 1
         for (int w = 0; w < NWD; ++w) {
-            mw[w] |= __shfl_xor_sync(msk, mw[w], 1);
-            mw[w] |= __shfl_xor_sync(msk, mw[w], 2);
-            mw[w] &= live_in(w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
+            uint32_t mw = 0;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int j = 32 * w + 4 * kk + q;
+                mw |= (FK(j, X) == key) ? (1u << (4 * kk + q)) : 0u;
+            }
+            mw |= __shfl_xor_sync(msk, mw, 1);
+            mw |= __shfl_xor_sync(msk, mw, 2);
+            mw &= live_in(w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
+            if (act) {
+                const uint32_t lo = mw & below_in(l, w), hi = mw & above_in(l, w);
+                if (lo) pred = 32 * w + 31 - __clz(lo);
+                if (hi && succ == NIL) succ = 32 * w + __ffs(hi) - 1;
+                nab += __popc(hi);
+                tot += __popc(mw);
+                for (uint32_t t = lo & (0x11111111u << q); t; t &= t - 1u) {
+                    const int m = 32 * w + __ffs(t) - 1;
+                    LK(m) += 1u << (10 * X);
+                }
+            }
         }
         if (!act) return;
-        int pred = NIL, succ = NIL, nab = 0, tot = 0;
-#pragma unroll
-        for (int w = 0; w < NWD; ++w) {
-            const uint32_t lo = mw[w] & below_in(l, w), hi = mw[w] & above_in(l, w);
-            if (lo) pred = 32 * w + 31 - __clz(lo);
-            if (hi && succ == NIL) succ = 32 * w + __ffs(hi) - 1;
-            nab += __popc(hi);
-            tot += __popc(mw[w]);
-        }
-#pragma unroll
-        for (int w = 0; w < NWD; ++w)
-            for (uint32_t t = mw[w] & below_in(l, w) & (0x11111111u << q); t; t &= t - 1u) {
-                const int m = 32 * w + __ffs(t) - 1;
-                LK(m) += 1u << (10 * X);
-            }
         if (owner(l)) {
             NXW(l) = set_byte(NXW(l), X, succ);
             PVW(l) = set_byte(PVW(l), X, pred);
@@ -538,7 +535,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         // R10 group prefix of the later counts: lane q sums its two rows of group g
         {
             uint32_t bu = 0, bv = 0, bwc = 0;
-#pragma unroll
+#pragma unroll 2
             for (int g = 0; g < NG; ++g) {
                 uint32_t s2 = LK(8 * g + q) + LK(8 * g + 4 + q);    // fields <= 2 x 127
                 s2 += __shfl_xor_sync(FULL, s2, 1);
@@ -636,8 +633,9 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         if (nC && !ok) draws = kf;
         c_draws += draws;
         // commit the flip (every quad takes part; `ok` gates the update)
-        commit_factor(ok, alpha, e_Y, e_ny);
-        commit_factor(ok, beta, e_Z, e_nz);
+        // (one inlined commit, looped over the two touched rows: code size)
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) commit_factor(ok, c ? beta : alpha, c ? e_Z : e_Y, c ? e_nz : e_ny);
 
         if (!ok) {
             // expand; continue
@@ -651,7 +649,9 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             flags |= 1u;
             // ---- R12 local reduction (exact skip), PAPER:310-313 acceptance
             // reduce (R15, exact skip) -- one loop so the reduction code is inlined once ----
-            const bool need_local = P::zero(e_ny) || P::zero(e_nz) || shares_two(alpha) || shares_two(beta);
+            bool need_local = P::zero(e_ny) || P::zero(e_nz);
+#pragma unroll 1
+            for (int c = 0; c < 2 && !need_local; ++c) need_local = shares_two(c ? beta : alpha);
 #pragma unroll 1
             for (int ph = 0; ph < 2; ++ph) {
                 const bool run = ph == 0 ? need_local : ((bern & 2u) && maybe);
