@@ -301,12 +301,11 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         if (nwl >= 2 && wl1 != h) { if (n2 == 0) x0 = wl1; else x1 = wl1; n2++; }
         wl0 = x0; wl1 = x1; nwl = n2;
         nnz_cur -= P::popd(FK(h, 0)) + P::popd(FK(h, 1)) + P::popd(FK(h, 2));
-        unlink_role(h, 0);
-        qsync();
-        unlink_role(h, 1);
-        qsync();
-        unlink_role(h, 2);
-        qsync();
+#pragma unroll 1
+        for (int X = 0; X < 3; ++X) {
+            unlink_role(h, X);
+            qsync();
+        }
         if (h != last) {
             // row `last` (the largest live index: the tail of each of its classes) moves
             // to h: in each class it moves down past its members in (h, last), which lose
@@ -357,56 +356,43 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             bool push = false;
             Row<P> merged;
             merged.u = merged.v = merged.w = 0;
+            int ib = 0, ie = 0;                  // rows i whose partners are searched
             if (local) {
                 if (nwl == 0) break;
                 const int t = wl0;
                 wl0 = wl1;
                 nwl--;
                 if (t >= r) continue;
-                if (row_zero(t)) {
-                    rm0 = t;
-                    c_zero++;
-                } else {
-                    const Row<P> rt = read_row(t);
-                    uint32_t cm[NWD];
-                    two_mask(t, -1, cm);
-                    int j = -1;
-#pragma unroll
-                    for (int w = 0; w < NWD; ++w)
-                        for (uint32_t c = cm[w]; c && j < 0; c &= c - 1u) {
-                            const int jj = 32 * w + __ffs(c) - 1;
-                            if (reducible<P>(rt, read_row(jj), merged)) j = jj;
-                        }
-                    if (j < 0) continue;
-                    lo = t < j ? t : j;
-                    wr = lo;
-                    rm0 = t < j ? j : t;
-                    c_merge++;
-                    if (has_zero(merged)) { rm1 = lo; c_zero++; } else push = true;
-                }
+                if (row_zero(t)) { rm0 = t; c_zero++; } else { ib = t; ie = t + 1; }
             } else {
                 for (int l = 0; l < r; ++l)
                     if (row_zero(l)) { rm0 = l; break; }
-                if (rm0 >= 0) {
-                    c_zero++;
-                } else {
-                    for (int i = 0; i < r && wr < 0; ++i) {
-                        uint32_t cm[NWD];
-                        two_mask(i, i, cm);
-                        const Row<P> ri = read_row(i);
+                if (rm0 >= 0) c_zero++; else { ib = 0; ie = r; }
+            }
+            if (rm0 < 0) {
+                // the first (i, j) in (i, j) order with reducible(row i, row j): local over
+                // all j != t, global over j > i (R12 / R15); one inlined search
+#pragma unroll 1
+                for (int i = ib; i < ie && wr < 0; ++i) {
+                    uint32_t cm[NWD];
+                    two_mask(i, local ? -1 : i, cm);
+                    const Row<P> ri = read_row(i);
 #pragma unroll
-                        for (int w = 0; w < NWD; ++w)
-                            for (uint32_t c = cm[w]; c && wr < 0; c &= c - 1u) {
-                                const int j = 32 * w + __ffs(c) - 1;
-                                if (!reducible<P>(ri, read_row(j), merged)) continue;
-                                wr = i;
-                                rm0 = j;
-                            }
-                    }
-                    if (wr < 0) break;
-                    c_merge++;
-                    if (has_zero(merged)) { rm1 = wr; c_zero++; }
+                    for (int w = 0; w < NWD; ++w)
+                        for (uint32_t c = cm[w]; c && wr < 0; c &= c - 1u) {
+                            const int j = 32 * w + __ffs(c) - 1;
+                            if (!reducible<P>(ri, read_row(j), merged)) continue;
+                            lo = i < j ? i : j;
+                            wr = lo;
+                            rm0 = i < j ? j : i;
+                        }
                 }
+                if (wr < 0) {
+                    if (local) continue;
+                    break;
+                }
+                c_merge++;
+                if (has_zero(merged)) { rm1 = lo; c_zero++; } else push = local;
             }
             if (wr >= 0) write_row(wr, merged, false);
 #pragma unroll 1
