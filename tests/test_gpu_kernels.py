@@ -16,7 +16,7 @@ from paper_2511_20317_b200.inputs import WORKLOADS, sample_walkers
 pytestmark = pytest.mark.gpu
 ZT, Z2 = 0, 1
 KERNELS = {"w32": "walk_w32", "h16": "walk_h16", "t1": "walk_t1", "q4": "walk_q4"}
-KERNEL_PREFIX = dict(KERNELS, ql="walk_ql")
+KERNEL_PREFIX = dict(KERNELS, ql="walk_ql", wm="walk_wm")
 
 
 @pytest.fixture(scope="module")
@@ -134,3 +134,18 @@ def test_ql_linked_class_kernel(fg, orc, case):
     ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
     _check(got, ref, None)
     assert g.stats()["verify_fail"] == 0
+
+
+@pytest.mark.parametrize("case", [((4, 4, 4), ZT, 96, 61, 2000), ((3, 3, 3), ZT, 33, 45, 3000), ((3, 4, 4), ZT, 64, 29, 2500)],
+                         ids=lambda c: f"{c[0]}-R{c[2]}")
+def test_wm_forced_for_zt_one_word(fg, orc, case):
+    """Z_T one-word formats with 33 <= R <= 128 default to walk_ql; the multi-row kernel
+    stays covered for them through FG_WALK_KERNEL=wm."""
+    (m, n, p), ring, R, W, steps = case
+    seed = 0x3A + R
+    g = _ctx(fg, "wm", m, n, p, ring, R, W)
+    g.seed_naive()
+    g.walk(steps, seed)
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
+    _check(got, ref, None)
