@@ -49,6 +49,7 @@ struct fg_ctx {
     fg_whdr *d_hdr;
     fg_qmeta *d_qmeta;
     DevMisc *d_misc;
+    uint32_t *d_task_done;   // walk_ql chunk flags, one per walker group of 8
     uint32_t qcap;
     cudaEvent_t ev0, ev1, ev2;
     // host bests
@@ -354,6 +355,7 @@ int fg_create(int m, int n, int p, int ring, int r_cap, int64_t num_walkers, int
     alloc((void **)&c->d_qplanes, words * c->qcap * 8);
     alloc((void **)&c->d_qmeta, sizeof(fg_qmeta) * c->qcap);
     alloc((void **)&c->d_misc, sizeof(DevMisc));
+    alloc((void **)&c->d_task_done, sizeof(uint32_t) * (size_t)((num_walkers + 7) / 8 + 1));
     alloc((void **)&c->d_pool, words * 8);
     if (rc == FG_OK && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
                         cudaEventCreate(&c->ev2) != cudaSuccess))
@@ -374,7 +376,7 @@ void fg_destroy(fg_ctx *c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaFree(c->d_cur); cudaFree(c->d_best); cudaFree(c->d_hdr); cudaFree(c->d_qplanes);
-    cudaFree(c->d_qmeta); cudaFree(c->d_misc); cudaFree(c->d_pool);
+    cudaFree(c->d_qmeta); cudaFree(c->d_misc); cudaFree(c->d_pool); cudaFree(c->d_task_done);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev2) cudaEventDestroy(c->ev2);
@@ -472,6 +474,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.q_planes = c->d_qplanes; a.q_meta = c->d_qmeta; a.q_count = &c->d_misc->q_count;
     a.q_cap = c->qcap; a.q_overflow = &c->d_misc->q_overflow; a.best_key = &c->d_misc->best_key;
     a.work_counter = &c->d_misc->work_counter;
+    a.task_done = c->d_task_done;
     a.dbg = getenv("FG_DBG") ? (uint32_t)strtoul(getenv("FG_DBG"), nullptr, 0) : 0u;
     a.dbgbuf = c->d_misc->dbgbuf;
     VerifyArgs v;
@@ -491,6 +494,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         CK(cudaMemsetAsync(&c->d_misc->best_key, 0xff, sizeof(unsigned long long), c->stream));
         CK(cudaMemsetAsync(&c->d_misc->q_count, 0, sizeof(uint32_t), c->stream));
         CK(cudaMemsetAsync(&c->d_misc->work_counter, 0, sizeof(unsigned long long), c->stream));
+        CK(cudaMemsetAsync(c->d_task_done, 0, sizeof(uint32_t) * (size_t)((c->W + 7) / 8 + 1), c->stream));
         CK(cudaEventRecord(c->ev0, c->stream));
         CK(fg_launch_walk(a.mode ? fg_kind_for_mode(c->kind) : c->kind, a, c->num_sms, c->stream));
         CK(cudaEventRecord(c->ev1, c->stream));

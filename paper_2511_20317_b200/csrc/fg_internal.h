@@ -58,6 +58,9 @@ struct WalkArgs {
     // local best key (R20): rank<<54 | additions<<36 | local walker index
     unsigned long long *best_key;
     unsigned long long *work_counter;   // dynamic walker queue, zeroed before each launch
+    uint32_t *task_done;                // walk_ql: per walker group, chunks stored (zeroed per launch)
+    uint32_t chunks;                    // walk_ql: step chunks per group (set by its launcher)
+    uint64_t chunk_steps;
     uint32_t mode;                      // 0 = Alg. 1 walk, 1 = naive-complexity minimisation (R24)
     uint32_t dbg;                       // debug switches (env FG_DBG), 0 in production
     uint32_t *dbgbuf;                   // 16 words of debug output (first error wins)
@@ -78,7 +81,7 @@ struct VerifyArgs {
 enum fg_kernel_kind { FG_K_NONE = 0, FG_K_W32_ZT_K16, FG_K_W32_ZT_K32, FG_K_W32_Z2_K32,
                       FG_K_WM_P16, FG_K_WM_P32, FG_K_WM_P64, FG_K_WM_Z2, FG_K_WM_Z64,
                       FG_K_H16_P16, FG_K_H16_P32, FG_K_H16_Z2, FG_K_T1_P16, FG_K_T1_Z2, FG_K_Q4_P16, FG_K_Q4_Z2, FG_K_QL_P16, FG_K_QL_Z2 };
-cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, cudaStream_t st);
+cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, cudaStream_t st);
 cudaError_t fg_launch_walk_t1(int kind, const WalkArgs &a, cudaStream_t st);
 cudaError_t fg_launch_walk_h16(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);

@@ -661,7 +661,7 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_Q4_P16:
     case FG_K_Q4_Z2: return fg_launch_walk_q4(kind, a, st);
     case FG_K_QL_P16:
-    case FG_K_QL_Z2: return fg_launch_walk_ql(kind, a, st);
+    case FG_K_QL_Z2: return fg_launch_walk_ql(kind, a, num_sms, st);
     default: return fg_launch_walk_multi(kind, fg_multi_ns(a.R), a, num_sms, st);
     }
 }

@@ -21,6 +21,7 @@
 //
 // Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
 // tests/test_gpu_kernels.py.
+#include <cstdlib>
 #include <type_traits>
 #include "fg_device.cuh"
 
@@ -47,7 +48,30 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     const int qb = lane & 28;
     const unsigned qm = 0xFu << qb;
     uint32_t *const S = smem + (threadIdx.x >> 5) * SLOTS * 8 + (lane >> 2);
-    const int64_t wk_raw = ((int64_t)blockIdx.x * (QL_THREADS / 32) + (threadIdx.x >> 5)) * 8 + (lane >> 2);
+    // Tasks = (walker group of 8, step chunk), handed out chunk-major by an atomic
+    // counter to persistent warps: a population of 1.26 waves costs ~1.3 chunk rounds
+    // instead of two full waves.  Chunk c of a group starts after chunk c-1 stored the
+    // group's state (task_done flag, fenced).  With one chunk this is one task per warp.
+    const int64_t n_groups = (a.num_walkers + 7) / 8;
+    const uint64_t n_tasks = (uint64_t)n_groups * a.chunks;
+#pragma unroll 1
+    for (;;) {
+    unsigned long long task = 0;
+    if (lane == 0) task = atomicAdd(a.work_counter, 1ull);
+    task = __shfl_sync(FULL, task, 0);
+    if (task >= n_tasks) break;
+    const int64_t grp = (int64_t)(task % (uint64_t)n_groups);
+    const uint32_t chunk = (uint32_t)(task / (uint64_t)n_groups);
+    if (chunk > 0) {
+        if (lane == 0)
+            while (*(volatile uint32_t *)(a.task_done + grp) < chunk) {}
+        __syncwarp();
+        __threadfence();
+    }
+    const uint64_t done_steps = (uint64_t)chunk * a.chunk_steps;
+    const uint64_t left = a.steps - done_steps;
+    const uint32_t nsteps_task = (uint32_t)(left < a.chunk_steps ? left : a.chunk_steps);
+    const int64_t wk_raw = grp * 8 + (lane >> 2);
     // a quad past the last walker stays in the warp (r = 0, no stores)
     const bool valid = wk_raw < a.num_walkers;
     const int64_t wk = valid ? wk_raw : 0;
@@ -500,7 +524,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         }
     };
 
-    const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
+    const uint32_t nsteps = nsteps_task;
 #pragma unroll 1
     for (uint32_t it = 0; it < nsteps; ++it, ++step) {
         // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1 and 3 block 2
@@ -693,10 +717,10 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         hp->step = step;
         hp->digest = digest;
         hp->best_adds = best_adds;
-        hp->cnt[FG_CNT_STEPS] += a.steps;
+        hp->cnt[FG_CNT_STEPS] += nsteps_task;
         hp->cnt[FG_CNT_DRAWS] += c_draws;
         hp->cnt[FG_CNT_FLIPS] += c_flips;
-        hp->cnt[FG_CNT_FLIP_FAIL] += a.steps - c_flips;
+        hp->cnt[FG_CNT_FLIP_FAIL] += nsteps_task - c_flips;
         hp->cnt[FG_CNT_EXPAND_OK] += c_eok;
         hp->cnt[FG_CNT_EXPAND_REJECT] += c_erej;
         hp->cnt[FG_CNT_MERGES] += c_merge;
@@ -709,6 +733,12 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         atomicMin(a.best_key, ((unsigned long long)best << 54) | ((unsigned long long)adds << 36) |
                                   (unsigned long long)wk);
     }
+    // this group's chunk is stored: release the next chunk
+    __syncwarp();
+    __threadfence();
+    if (lane == 0) atomicExch(a.task_done + grp, chunk + 1);
+    __syncwarp();
+    }   // task loop
 #undef FK
 #undef NXW
 #undef PVW
@@ -717,7 +747,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
 }
 
 template <class P, int NWD>
-cudaError_t launch_ql(const WalkArgs &a, cudaStream_t st)
+cudaError_t launch_ql(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     constexpr int RM = 32 * NWD;
     const size_t smem = (size_t)(6 * RM + 2 * (RM / 8)) * 8 * 4 * (QL_THREADS / 32);
@@ -727,27 +757,40 @@ cudaError_t launch_ql(const WalkArgs &a, cudaStream_t st)
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int64_t per_block = (QL_THREADS / 32) * 8;
-    const int64_t blocks = (a.num_walkers + per_block - 1) / per_block;
-    walk_ql<P, NWD><<<(unsigned)blocks, QL_THREADS, smem, st>>>(a);
+    int bps = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_ql<P, NWD>, QL_THREADS, smem);
+    if (e != cudaSuccess) return e;
+    if (bps < 1) bps = 1;
+    const int64_t resident = (int64_t)num_sms * bps;            // warps (1-warp CTAs)
+    const int64_t groups = (a.num_walkers + 7) / 8;
+    WalkArgs b = a;
+    // one wave: one task per warp; more: 8 step chunks per group over persistent warps
+    b.chunks = (groups > resident && a.steps >= 64) ? 8u : 1u;
+    if (const char *ev = getenv("FG_QL_CHUNKS")) {               // tests: force chunking
+        const long k = strtol(ev, nullptr, 10);
+        if (k >= 1 && k <= 64) b.chunks = (uint32_t)k;
+    }
+    b.chunk_steps = (a.steps + b.chunks - 1) / b.chunks;
+    const int64_t blocks = groups < resident ? groups : resident;
+    walk_ql<P, NWD><<<(unsigned)blocks, QL_THREADS, smem, st>>>(b);
     return cudaGetLastError();
 }
 
 template <class P>
-cudaError_t launch_ql_r(const WalkArgs &a, cudaStream_t st)
+cudaError_t launch_ql_r(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
-    if (a.R <= 64) return launch_ql<P, 2>(a, st);
-    if (a.R <= 96) return launch_ql<P, 3>(a, st);
-    return launch_ql<P, 4>(a, st);
+    if (a.R <= 64) return launch_ql<P, 2>(a, num_sms, st);
+    if (a.R <= 96) return launch_ql<P, 3>(a, num_sms, st);
+    return launch_ql<P, 4>(a, num_sms, st);
 }
 
 }  // namespace
 
-cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, cudaStream_t st)
+cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     switch (kind) {
-    case FG_K_QL_P16: return launch_ql_r<P16>(a, st);
-    case FG_K_QL_Z2: return launch_ql_r<PZ2>(a, st);
+    case FG_K_QL_P16: return launch_ql_r<P16>(a, num_sms, st);
+    case FG_K_QL_Z2: return launch_ql_r<PZ2>(a, num_sms, st);
     default: return cudaErrorInvalidValue;
     }
 }

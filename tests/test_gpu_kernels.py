@@ -149,3 +149,25 @@ def test_wm_forced_for_zt_one_word(fg, orc, case):
     got = g.get_walkers()
     ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
     _check(got, ref, None)
+
+
+def test_ql_chunked_tasks(fg, orc):
+    """walk_ql's persistent (walker group, step chunk) tasks: forcing 3 chunks per group
+    (FG_QL_CHUNKS) leaves every trajectory unchanged -- the chunks hand the state over
+    through HBM in order."""
+    (m, n, p), ring, R, W, steps = (4, 4, 4), ZT, 96, 83, 1500
+    old = os.environ.get("FG_QL_CHUNKS")
+    os.environ["FG_QL_CHUNKS"] = "3"
+    try:
+        g = _ctx(fg, "ql", m, n, p, ring, R, W)
+        g.seed_naive()
+        g.walk(steps, 0xC4C4)
+    finally:
+        if old is None:
+            del os.environ["FG_QL_CHUNKS"]
+        else:
+            os.environ["FG_QL_CHUNKS"] = old
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, 0xC4C4)
+    _check(got, ref, None)
+    assert np.all(got["step"] == steps)
