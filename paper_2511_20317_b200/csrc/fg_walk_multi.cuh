@@ -40,6 +40,10 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
     const uint64_t seed = a.seed;
     const uint32_t kf = a.k_flip;
     constexpr int PLANE = NS * 32;
+    // per-row slot loops: fully unrolled up to 8 slots; rolled above (the class counts then
+    // live in local memory) -- the fully unrolled kernel for NS = 13 is 39k instructions
+    // and stalls on instruction fetch
+    constexpr int UNS = NS > 8 ? 1 : NS;
 
     auto grab = [&]() -> int64_t {
         unsigned long long v = 0;
@@ -98,7 +102,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
         auto pair_update = [&](int t, F bu, F bv, F bw_, int sign) {
             const F nbw = P::neg(bw_);
             const bool zu = P::zero(bu), zv = P::zero(bv), zw = P::zero(bw_);
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s) {
                 const int l = lane * NS + s;
                 if (l < t) {
@@ -112,7 +116,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
             const F nbw = P::neg(bw_);
             const bool zu = P::zero(bu), zv = P::zero(bv), zw = P::zero(bw_);
             uint32_t acc = 0;
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s) {
                 const int l = lane * NS + s;
                 if (l > t && l < r) acc += cls3(s, bu, bv, bw_, nbw, zu, zv, zw);
@@ -120,17 +124,17 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
             acc = (uint32_t)__reduce_add_sync(FULL, acc & 1023u) |
                   ((uint32_t)__reduce_add_sync(FULL, (acc >> 10) & 1023u) << 10) |
                   ((uint32_t)__reduce_add_sync(FULL, acc >> 20) << 20);
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s)
                 if (lane * NS + s == t) cnt[s] = acc;
         };
         auto set_cnt = [&](int t, uint32_t v) {
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s)
                 if (lane * NS + s == t) cnt[s] = v;
         };
         auto recount = [&]() {
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s) cnt[s] = 0;
             for (int t = 1; t < r; ++t) pair_update(t, fat(0, t), fat(1, t), fat(2, t), +1);
         };
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
             const bool classdiff = X == 2 ? !P::eq(P::abs(ov), P::abs(nv)) : !P::eq(ov, nv);
             if (classdiff || zo != zn) {
                 uint32_t above = 0;
-#pragma unroll
+#pragma unroll UNS
                 for (int s = 0; s < NS; ++s) {
                     const int l = lane * NS + s;
                     const F x = own(X, s);
@@ -152,7 +156,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     above += (l > t && l < r) ? mn : 0u;
                 }
                 const uint32_t tot = (uint32_t)__reduce_add_sync(FULL, above);
-#pragma unroll
+#pragma unroll UNS
                 for (int s = 0; s < NS; ++s)
                     if (lane * NS + s == t) cnt[s] = (cnt[s] & ~(1023u << (10 * X))) | (tot << (10 * X));
             }
@@ -252,7 +256,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
         auto first_reducible = [&](const Row<P> &rt, int t, int lmin, Row<P> &merged) -> int {
             int found = 0x7fffffff;
             Row<P> mg = rt;
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s) {
                 const int l = lane * NS + s;
                 if (l < r && l != t && l >= lmin && found == 0x7fffffff) {
@@ -306,7 +310,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
         auto slow_reduce_all = [&]() {
             for (;;) {
                 int zfirst = 0x7fffffff;
-#pragma unroll
+#pragma unroll UNS
                 for (int s = 0; s < NS; ++s) {
                     const int l = lane * NS + s;
                     if (l < r && zfirst == 0x7fffffff &&
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                         const int d = (int)((dset >> (10 * k)) & 1023u);
                         const Row<P> rd = row_at(d);
                         int key = 0x7fffffff;
-#pragma unroll
+#pragma unroll UNS
                         for (int s = 0; s < NS; ++s) {
                             const int l = lane * NS + s;
                             if (l < r && l != d) {
@@ -441,7 +445,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
 
         auto nnz_all = [&]() -> int {
             int v = 0;
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s)
                 if (lane * NS + s < r) v += P::popd(own(0, s)) + P::popd(own(1, s)) + P::popd(own(2, s));
             return __reduce_add_sync(FULL, v);
@@ -472,7 +476,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
 
             // ---- R10 counts: lane sums (3 x 21 bits) + warp scan ----
             uint64_t lsum = 0;
-#pragma unroll
+#pragma unroll UNS
             for (int s = 0; s < NS; ++s)
                 lsum += (uint64_t)(cnt[s] & 1023u) | ((uint64_t)((cnt[s] >> 10) & 1023u) << 21) |
                         ((uint64_t)(cnt[s] >> 20) << 42);
@@ -516,7 +520,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     int sl = 0;
                     uint32_t q2 = 0, cum = 0;
                     bool found = false;
-#pragma unroll
+#pragma unroll UNS
                     for (int s = 0; s < NS; ++s) {
                         const uint32_t f = (cnt[s] >> (10 * X)) & 1023u;
                         if (!found && cum + f > q1) { found = true; sl = s; q2 = q1 - cum; }
@@ -529,7 +533,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     const F xi = fat(X, i);
                     const F nxi = P::neg(xi);
                     uint32_t bits = 0;
-#pragma unroll
+#pragma unroll UNS
                     for (int s = 0; s < NS; ++s) {
                         const int l = lane * NS + s;
                         const F xl = own(X, s);
@@ -628,7 +632,7 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     const F nwa = P::neg(ra.w), nwb = P::neg(rb.w);
                     bool need = has_zero(ra) || has_zero(rb);
                     bool hit = false;
-#pragma unroll
+#pragma unroll UNS
                     for (int s = 0; s < NS; ++s) {
                         const int l = lane * NS + s;
                         if (l < r) {
