@@ -208,9 +208,15 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     };
     // join the class of `key` in role X (FK(l,X) already holds key, written by owner(l)):
     // one compare pass over the rows, split over the quad.  Collective over msk.
-    auto link_role = [&](auto wtag, int l, int X, uint32_t key, bool act) __attribute__((always_inline)) {
+    // With WARP it also reports whether some row other than l and `excl` shares two factors
+    // with row l after the change (R12's skip test): the same pass compares the rows with
+    // l's other two class keys.
+    auto link_role = [&](auto wtag, int l, int X, uint32_t key, bool act, int excl, bool &two) __attribute__((always_inline)) {
         constexpr bool WARP = decltype(wtag)::value;
         const unsigned msk = WARP ? FULL : qm;
+        const int O1 = X == 2 ? 0 : X + 1, O2 = X == 0 ? 2 : X - 1;
+        const uint32_t k1 = WARP ? FK(l, O1) : 0u, k2 = WARP ? FK(l, O2) : 0u;
+        two = false;
         // one mask word (32 rows) per iteration, not unrolled: a compact loop body keeps
         // the instruction stream small (the unrolled 24-row pass missed the i-cache)
         int pred = NIL, succ = NIL, nab = 0, tot = 0;
@@ -224,7 +230,24 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             }
             mw |= __shfl_xor_sync(msk, mw, 1);
             mw |= __shfl_xor_sync(msk, mw, 2);
-            mw &= live_in(w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
+            const uint32_t keep = live_in(w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
+            mw &= keep;
+            if (WARP) {
+                uint32_t m1 = 0, m2 = 0;
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int j = 32 * w + 4 * kk + q;
+                    m1 |= (FK(j, O1) == k1) ? (1u << (4 * kk + q)) : 0u;
+                    m2 |= (FK(j, O2) == k2) ? (1u << (4 * kk + q)) : 0u;
+                }
+                m1 |= __shfl_xor_sync(msk, m1, 1);
+                m2 |= __shfl_xor_sync(msk, m2, 1);
+                m1 |= __shfl_xor_sync(msk, m1, 2);
+                m2 |= __shfl_xor_sync(msk, m2, 2);
+                const uint32_t ex = ((excl >> 5) == w && excl >= 0) ? (1u << (excl & 31)) : 0u;
+                const uint32_t k = keep & ~ex;
+                two = two || ((((mw & (m1 | m2)) | (m1 & m2)) & k) != 0u);
+            }
             if (act) {
                 const uint32_t lo = mw & below_in(l, w), hi = mw & above_in(l, w);
                 if (lo) pred = 32 * w + 31 - __clz(lo);
@@ -249,13 +272,13 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     };
     // row l's X key becomes `key` (fresh: l is in no X class yet).  Collective over the
     // quad (wtag false) or the warp (wtag true: every quad calls it, `act` gates it).
-    auto set_class = [&](auto wtag, int l, int X, uint32_t key, bool fresh, bool act) __attribute__((always_inline)) {
+    auto set_class = [&](auto wtag, int l, int X, uint32_t key, bool fresh, bool act, int excl, bool &two) __attribute__((always_inline)) {
         constexpr bool WARP = decltype(wtag)::value;
         const unsigned msk = WARP ? FULL : qm;
         if (act && !fresh) unlink_role(l, X);
         __syncwarp(msk);
         if (act && owner(l)) FK(l, X) = key;
-        link_role(wtag, l, X, key, act);
+        link_role(wtag, l, X, key, act, excl, two);
         __syncwarp(msk);
     };
     // store a whole (normalised) row; only changed keys pay a class update.  Quad.
@@ -273,14 +296,15 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         for (int X = 0; X < 3; ++X) {
             const F kX = X == 0 ? x.u : (X == 1 ? x.v : P::abs(x.w));
             const F oX = X == 0 ? o0 : (X == 1 ? o1 : o2);
-            if (fresh || kX != oX) set_class(std::false_type{}, l, X, kX, fresh, true);
+            bool dummy;
+            if (fresh || kX != oX) set_class(std::false_type{}, l, X, kX, fresh, true, -1, dummy);
         }
         set_wbit(l, P::first_neg(x.w));
         qsync();
     };
     // the flip commit: factor Y of row l becomes val (actual sign) if `act`; only this
     // factor can trigger PAPER:429 (R6).  Whole-warp collective.
-    auto commit_factor = [&](bool act, int l, int Y, F val) __attribute__((always_inline)) {
+    auto commit_factor = [&](bool act, int l, int Y, F val, int excl, bool &two) __attribute__((always_inline)) {
         const F old = FK(l, Y);
         const bool fn = P::first_neg(val);
         const F key = Y == 2 ? P::abs(val) : (fn ? P::neg(val) : val);
@@ -288,17 +312,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             nnz_cur += P::popd(val) - P::popd(old);
             set_wbit(l, Y == 2 ? (uint32_t)fn : (wbit(l) ^ (uint32_t)fn));
         }
-        set_class(std::true_type{}, l, Y, key, false, act && key != old);
-    };
-    // does a live row other than l share two factors with row l (R13's precondition)?
-    // Such a row is in l's U class (U+V, U+W) or its V class (V+W).
-    auto shares_two = [&](int l) __attribute__((always_inline)) -> bool {
-        const F v = FK(l, 1), w = FK(l, 2);
-        for (int m = nxt(l, 0); m != NIL; m = nxt(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w) return true;
-        for (int m = prv(l, 0); m != NIL; m = prv(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w) return true;
-        for (int m = nxt(l, 1); m != NIL; m = nxt(m, 1)) if (FK(m, 2) == w) return true;
-        for (int m = prv(l, 1); m != NIL; m = prv(m, 1)) if (FK(m, 2) == w) return true;
-        return false;
+        set_class(std::true_type{}, l, Y, key, false, act && key != old, excl, two);
     };
     // rows j (> lmin) sharing two factors with row l, as a row mask
     auto two_mask = [&](int l, int lmin, uint32_t (&cm)[NWD]) {
@@ -644,8 +658,13 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         c_draws += draws;
         // commit the flip (every quad takes part; `ok` gates the update)
         // (one inlined commit, looped over the two touched rows: code size)
+        bool two_ab = false;            // a touched row shares two factors with another row
 #pragma unroll 1
-        for (int c = 0; c < 2; ++c) commit_factor(ok, c ? beta : alpha, c ? e_Z : e_Y, c ? e_nz : e_ny);
+        for (int c = 0; c < 2; ++c) {
+            bool two;
+            commit_factor(ok, c ? beta : alpha, c ? e_Z : e_Y, c ? e_nz : e_ny, c ? -1 : beta, two);
+            two_ab = two_ab || two;
+        }
 
         if (!ok) {
             // expand; continue
@@ -659,9 +678,11 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             flags |= 1u;
             // ---- R12 local reduction (exact skip), PAPER:310-313 acceptance
             // reduce (R15, exact skip) -- one loop so the reduction code is inlined once ----
-            bool need_local = P::zero(e_ny) || P::zero(e_nz);
-#pragma unroll 1
-            for (int c = 0; c < 2 && !need_local; ++c) need_local = shares_two(c ? beta : alpha);
+            // alpha's test ran before beta's commit and left beta out: the pair itself is
+            // checked here (class keys compare W up to sign)
+            const int same = (FK(alpha, 0) == FK(beta, 0)) + (FK(alpha, 1) == FK(beta, 1)) +
+                             (FK(alpha, 2) == FK(beta, 2));
+            const bool need_local = P::zero(e_ny) || P::zero(e_nz) || two_ab || same >= 2;
 #pragma unroll 1
             for (int ph = 0; ph < 2; ++ph) {
                 const bool run = ph == 0 ? need_local : ((bern & 2u) && maybe);
