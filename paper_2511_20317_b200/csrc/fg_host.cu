@@ -50,6 +50,7 @@ struct fg_ctx {
     fg_qmeta *d_qmeta;
     DevMisc *d_misc;
     uint32_t *d_task_done;   // walk_ql chunk flags, one per walker group of 8
+    uint32_t *d_ql_img;      // walk_ql: shared-memory image per walker between chunks
     uint32_t qcap;
     cudaEvent_t ev0, ev1, ev2;
     // host bests
@@ -356,6 +357,8 @@ int fg_create(int m, int n, int p, int ring, int r_cap, int64_t num_walkers, int
     alloc((void **)&c->d_qmeta, sizeof(fg_qmeta) * c->qcap);
     alloc((void **)&c->d_misc, sizeof(DevMisc));
     alloc((void **)&c->d_task_done, sizeof(uint32_t) * (size_t)((num_walkers + 7) / 8 + 1));
+    if (kind == FG_K_QL_P16 || kind == FG_K_QL_Z2)   // 6 R + R / 4 slots + 5 scalars, R <= 128
+        alloc((void **)&c->d_ql_img, sizeof(uint32_t) * (size_t)(6 * 128 + 32 + 5) * num_walkers);
     alloc((void **)&c->d_pool, words * 8);
     if (rc == FG_OK && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
                         cudaEventCreate(&c->ev2) != cudaSuccess))
@@ -376,7 +379,7 @@ void fg_destroy(fg_ctx *c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaFree(c->d_cur); cudaFree(c->d_best); cudaFree(c->d_hdr); cudaFree(c->d_qplanes);
-    cudaFree(c->d_qmeta); cudaFree(c->d_misc); cudaFree(c->d_pool); cudaFree(c->d_task_done);
+    cudaFree(c->d_qmeta); cudaFree(c->d_misc); cudaFree(c->d_pool); cudaFree(c->d_task_done); cudaFree(c->d_ql_img);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev2) cudaEventDestroy(c->ev2);
@@ -475,6 +478,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.q_cap = c->qcap; a.q_overflow = &c->d_misc->q_overflow; a.best_key = &c->d_misc->best_key;
     a.work_counter = &c->d_misc->work_counter;
     a.task_done = c->d_task_done;
+    a.ql_img = c->d_ql_img;
     a.dbg = getenv("FG_DBG") ? (uint32_t)strtoul(getenv("FG_DBG"), nullptr, 0) : 0u;
     a.dbgbuf = c->d_misc->dbgbuf;
     VerifyArgs v;

@@ -61,6 +61,7 @@ struct WalkArgs {
     uint32_t *task_done;                // walk_ql: per walker group, chunks stored (zeroed per launch)
     uint32_t chunks;                    // walk_ql: step chunks per group (set by its launcher)
     uint64_t chunk_steps;
+    uint32_t *ql_img;                   // walk_ql: per-walker shared-memory image between chunks
     uint32_t mode;                      // 0 = Alg. 1 walk, 1 = naive-complexity minimisation (R24)
     uint32_t dbg;                       // debug switches (env FG_DBG), 0 in production
     uint32_t *dbgbuf;                   // 16 words of debug output (first error wins)

@@ -120,11 +120,26 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     };
     auto live_in = [&](int w) __attribute__((always_inline)) -> uint32_t { return below_in(r, w); };
 
-    // ---------------- load the walker (own rows) ----------------
+    // ---------------- load the walker ----------------
+    // chunk 0 of a launch builds the class structure from the plane layout; a later chunk
+    // restores the shared-memory image and scalars the previous chunk saved (ql_img)
     int nnz_cur = 0;
+    uint32_t nCU = 0, nCV = 0, nCW = 0;     // flip-candidate pairs per role (R10)
+    bool maybe = true;                      // R15: a full reduce_all may find work
+    constexpr int IMG = SLOTS + 5;          // image words per walker
+    uint32_t *const img = a.ql_img ? a.ql_img + (size_t)wk * IMG : nullptr;
+    const bool resume = chunk > 0 && img != nullptr && valid;
+    if (resume) {
+#pragma unroll 1
+        for (int k = q; k < SLOTS; k += 4) S[k * 8] = img[k];
+        nnz_cur = (int)img[SLOTS];
+        nCU = img[SLOTS + 1]; nCV = img[SLOTS + 2]; nCW = img[SLOTS + 3];
+        maybe = img[SLOTS + 4] != 0u;
+        qsync();
+    }
     uint32_t own_sign = 0;                       // W signs of own rows (bit l / 4)
 #pragma unroll 1
-    for (int l = q; l < RM; l += 4) {
+    for (int l = q; l < RM && !resume; l += 4) {
         F u = 0, v = 0, w = 0;
         if (l < r) {
             u = P::make(cp[0 * R + l], cp[1 * R + l]);
@@ -135,18 +150,19 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         own_sign |= (uint32_t)P::first_neg(w) << (l >> 2);
         FK(l, 0) = u; FK(l, 1) = v; FK(l, 2) = P::abs(w);
     }
-    nnz_cur += __shfl_xor_sync(qm, nnz_cur, 1);
-    nnz_cur += __shfl_xor_sync(qm, nnz_cur, 2);
+    if (!resume) {
+        nnz_cur += __shfl_xor_sync(qm, nnz_cur, 1);
+        nnz_cur += __shfl_xor_sync(qm, nnz_cur, 2);
+    }
     qsync();
 
-    // class links and later counts from scratch (once per launch): own rows
-    uint32_t nCU = 0, nCV = 0, nCW = 0;     // flip-candidate pairs per role (R10)
+    // class links and later counts from scratch (chunk 0): own rows
     auto addn = [&](int X, int v) __attribute__((always_inline)) {
         nCU += X == 0 ? (uint32_t)v : 0u;
         nCV += X == 1 ? (uint32_t)v : 0u;
         nCW += X == 2 ? (uint32_t)v : 0u;
     };
-    {
+    if (!resume) {
         uint32_t pu = 0, pv_ = 0, pw = 0;
 #pragma unroll 1
         for (int l = q; l < RM; l += 4) {
@@ -175,7 +191,6 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         nCU = pu; nCV = pv_; nCW = pw;
         qsync();
     }
-    bool maybe = true;     // R15: a full reduce_all may find work
 
     auto fac = [&](int l, int X) __attribute__((always_inline)) -> F {
         const F k = FK(l, X);
@@ -724,6 +739,17 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         digest ^= digest >> 32;
     }
 
+    // ---------------- save the image for the next chunk of this launch ----------------
+    if (valid && img && chunk + 1 < a.chunks) {
+        qsync();
+#pragma unroll 1
+        for (int k = q; k < SLOTS; k += 4) img[k] = S[k * 8];
+        if (q == 0) {
+            img[SLOTS] = (uint32_t)nnz_cur;
+            img[SLOTS + 1] = nCU; img[SLOTS + 2] = nCV; img[SLOTS + 3] = nCW;
+            img[SLOTS + 4] = maybe ? 1u : 0u;
+        }
+    }
     // ---------------- store own rows; best additions from the best rows in HBM ----------------
     __syncwarp();
     if (valid) store_rows(a.cur + (size_t)wk * FG_PLANES * R);
