@@ -596,15 +596,14 @@ int fg_pick_kernel(int ring, int maxlen, int R)
         if (h16) return FG_K_H16_Z2;
         return w32 ? FG_K_W32_Z2_K32 : (t1 ? FG_K_T1_Z2 : FG_K_Q4_Z2);
     }
-    // 33 <= R <= 128, one-word factors: the linked-class quad kernel (fg_walk_ql.cu) is
-    // the default for Z_T (faster than walk_wm on (4,4,4), profiles/r01_bench_multi.txt);
-    // for Z_2 (larger classes, longer list walks) walk_wm stays faster.  FG_WALK_KERNEL=ql
-    // / wm force one or the other.
+    // 33 <= R <= 128, one-word factors: the linked-class quad kernel (fg_walk_ql.cu),
+    // faster than walk_wm on (4,4,4) Z_T and Z_2 (profiles/r01_bench_multi.txt);
+    // FG_WALK_KERNEL=wm forces the one-walker-per-warp multi-row kernel.
     const char *env = getenv("FG_WALK_KERNEL");
-    const bool ql = env && strcmp(env, "ql") == 0, wm = env && strcmp(env, "wm") == 0;
+    const bool wm = env && strcmp(env, "wm") == 0;
     if (R <= 128 && !wm) {
         if (ring == FG_ZT && maxlen <= 16) return FG_K_QL_P16;
-        if (ql && ring == FG_Z2 && maxlen <= 32) return FG_K_QL_Z2;
+        if (ring == FG_Z2 && maxlen <= 32) return FG_K_QL_Z2;
     }
     return fg_multi_kind(ring, maxlen, R);
 }

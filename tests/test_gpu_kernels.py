@@ -136,10 +136,11 @@ def test_ql_linked_class_kernel(fg, orc, case):
     assert g.stats()["verify_fail"] == 0
 
 
-@pytest.mark.parametrize("case", [((4, 4, 4), ZT, 96, 61, 2000), ((3, 3, 3), ZT, 33, 45, 3000), ((3, 4, 4), ZT, 64, 29, 2500)],
-                         ids=lambda c: f"{c[0]}-R{c[2]}")
-def test_wm_forced_for_zt_one_word(fg, orc, case):
-    """Z_T one-word formats with 33 <= R <= 128 default to walk_ql; the multi-row kernel
+@pytest.mark.parametrize("case", [((4, 4, 4), ZT, 96, 61, 2000), ((3, 3, 3), ZT, 33, 45, 3000), ((3, 4, 4), ZT, 64, 29, 2500),
+                                  ((4, 4, 4), Z2, 96, 40, 2000), ((3, 3, 3), Z2, 64, 45, 2500)],
+                         ids=lambda c: f"{c[0]}-{'zt' if c[1] == ZT else 'z2'}-R{c[2]}")
+def test_wm_forced_for_one_word(fg, orc, case):
+    """One-word formats with 33 <= R <= 128 default to walk_ql; the multi-row kernel
     stays covered for them through FG_WALK_KERNEL=wm."""
     (m, n, p), ring, R, W, steps = case
     seed = 0x3A + R

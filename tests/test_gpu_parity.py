@@ -234,9 +234,9 @@ MULTI_CASES = [
 def test_multi_row_kernel_parity(fg, orc, case):
     (m, n, p), ring, R, W, k, steps = case
     g = _ctx(fg, m, n, p, ring, R, W, base=77)
-    # Z_T one-word factors with R <= 128 run on the linked-class quad kernel (walk_ql)
-    assert g.kernel_name.startswith("walk_ql" if ring == ZT and R <= 128 and max(m * n, n * p, p * m) <= 16
-                                    else "walk_wm")
+    # one-word factors with R <= 128 run on the linked-class quad kernel (walk_ql)
+    maxlen = max(m * n, n * p, p * m)
+    assert g.kernel_name.startswith("walk_ql" if R <= 128 and maxlen <= (16 if ring == ZT else 32) else "walk_wm")
     g.seed_naive()
     seed = 0x2511203170000000 + 2 + ring
     half = steps // 2
