@@ -618,11 +618,13 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                         }
                     }
                 }
+            }
+            // expand (R16) runs last on both paths: one inlined copy
+            uint32_t exp_flag = 0;
+            if (cmode) {
             } else if (!ok) {
-                const bool ex = expand();
-                bump(RC_EOK, ex);
-                bump(RC_EREJ, !ex);
-                flags |= 2u | (ex ? 64u : 0u);
+                // expand; continue
+                exp_flag = 2u;
             } else {
                 c_flips++;
                 flags |= 1u;
@@ -684,12 +686,13 @@ __global__ void __launch_bounds__(32) walk_wm(WalkArgs a)
                     if (dover || nD > 0) slow_reduce_all();
                 }
                 // ---- PAPER:319-321 expand ----
-                if ((bern & 4u) && r <= best + a.slack) {
-                    const bool ex = expand();
-                    flags |= 32u | (ex ? 64u : 0u);
-                    bump(RC_EOK, ex);
-                    bump(RC_EREJ, !ex);
-                }
+                if ((bern & 4u) && r <= best + a.slack) exp_flag = 32u;
+            }
+            if (exp_flag) {
+                const bool ex = expand();
+                flags |= exp_flag | (ex ? 64u : 0u);
+                bump(RC_EOK, ex);
+                bump(RC_EREJ, !ex);
             }
             const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)(cmode ? (best_adds & 1023) : best) << 10) |
                                 ((uint64_t)flags << 20) | ((uint64_t)alpha << 32) |
