@@ -43,7 +43,8 @@ struct fg_ctx {
     int64_t W, id_base;
     int device, num_sms;
     cudaStream_t stream;
-    bool seeded;
+    bool seeded;                       // every walker in [0, W) holds a scheme
+    std::vector<std::pair<int64_t, int64_t>> covered;   // seeded walker ranges, merged
     // device
     uint64_t *d_cur, *d_best, *d_qplanes, *d_pool;
     fg_whdr *d_hdr;
@@ -226,7 +227,22 @@ int replicate(fg_ctx *c, uint64_t *dst, const uint64_t *src_dev, int64_t words, 
 }
 
 int recompute_local_best(fg_ctx *c);
-int refresh_local_best(fg_ctx *c, unsigned long long key);
+int refresh_local_best(fg_ctx *c, unsigned long long key, bool reset);
+
+// record [w0, w1) as seeded; the ctx is walkable once the ranges cover [0, W)
+void mark_covered(fg_ctx *c, int64_t w0, int64_t w1)
+{
+    auto &v = c->covered;
+    v.push_back({w0, w1});
+    std::sort(v.begin(), v.end());
+    std::vector<std::pair<int64_t, int64_t>> out;
+    for (const auto &x : v) {
+        if (!out.empty() && x.first <= out.back().second) out.back().second = std::max(out.back().second, x.second);
+        else out.push_back(x);
+    }
+    v.swap(out);
+    c->seeded = v.size() == 1 && v[0].first == 0 && v[0].second == c->W;
+}
 
 int seed_planes(fg_ctx *c, const uint64_t *planes, int rank, int64_t w0, int64_t w1)
 {
@@ -253,39 +269,59 @@ int seed_planes(fg_ctx *c, const uint64_t *planes, int rank, int64_t w0, int64_t
     CK(cudaFreeAsync(tmph, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (rc != FG_OK) return rc;
-    c->seeded = true;
-    return recompute_local_best(c);
+    mark_covered(c, w0, w1);
+    // the local best is defined once every walker holds a scheme (a partial
+    // seed must not let zeroed headers of unseeded walkers into the best key)
+    return c->seeded ? recompute_local_best(c) : FG_OK;
 }
 
-int refresh_local_best(fg_ctx *c, unsigned long long key)
+// best key over the walkers' best schemes on the device, skipping walkers whose
+// verification failed (bestkey_kernel)
+int device_best_key(fg_ctx *c, unsigned long long *key)
+{
+    CK(cudaMemsetAsync(&c->d_misc->best_key, 0xff, sizeof(unsigned long long), c->stream));
+    CK(fg_launch_bestkey(c->d_best, c->d_hdr, c->W, c->R, c->m * c->p, &c->d_misc->best_key, c->stream));
+    c->st_launches++;
+    *key = ~0ull;
+    CK(cudaMemcpyAsync(key, &c->d_misc->best_key, sizeof(*key), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return FG_OK;
+}
+
+// Build the record of the walker the key names and make it the local best if it is
+// better (R20), or unconditionally with `reset` (seed / load / restart).  The record
+// is checked against the Brent equations first (R19: an unverified scheme is never
+// stored): a failure returns FG_E_INVALID_SCHEME and leaves the local best alone.
+int refresh_local_best(fg_ctx *c, unsigned long long key, bool reset)
 {
     const int64_t words = (int64_t)FG_PLANES * c->R;
     const int64_t wk = (int64_t)(key & ((1ull << 36) - 1));
+    if (reset) ((RecHdr *)c->local_rec.data())->valid = 0;
     if (key == ~0ull || wk >= c->W) return FG_OK;
-    RecHdr *lh = (RecHdr *)c->local_rec.data();
-    uint64_t *pl = (uint64_t *)(c->local_rec.data() + sizeof(RecHdr));
+    std::vector<unsigned char> cand(rec_bytes(c->R), 0);
+    RecHdr *ch = (RecHdr *)cand.data();
+    uint64_t *pl = (uint64_t *)(cand.data() + sizeof(RecHdr));
     CK(cudaMemcpyAsync(pl, c->d_best + wk * words, words * sizeof(uint64_t), cudaMemcpyDeviceToHost,
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    memset(lh, 0, sizeof(*lh));
-    lh->magic = REC_MAGIC; lh->m = c->m; lh->n = c->n; lh->p = c->p; lh->ring = c->ring;
-    lh->r_cap = c->R; lh->rank = (int)(key >> 54);
-    lh->additions = additions_planes(c->m, c->p, pl, c->R, lh->rank);
-    lh->walker_id = c->id_base + wk; lh->valid = 1;
+    ch->magic = REC_MAGIC; ch->m = c->m; ch->n = c->n; ch->p = c->p; ch->ring = c->ring;
+    ch->r_cap = c->R; ch->rank = (int)(key >> 54);
+    ch->additions = additions_planes(c->m, c->p, pl, c->R, ch->rank);
+    ch->walker_id = c->id_base + wk; ch->valid = 1;
+    int32_t ff[3];
+    if (ch->rank < 1 || verify_planes(c->m, c->n, c->p, c->ring, pl, c->R, ch->rank, ff) != FG_OK)
+        return FG_E_INVALID_SCHEME;
+    if (rec_better(ch, (const RecHdr *)c->local_rec.data())) c->local_rec.swap(cand);
     return FG_OK;
 }
 
 // local best over every walker's best scheme, from the device
 int recompute_local_best(fg_ctx *c)
 {
-    CK(cudaMemsetAsync(&c->d_misc->best_key, 0xff, sizeof(unsigned long long), c->stream));
-    CK(fg_launch_bestkey(c->d_best, c->d_hdr, c->W, c->R, c->m * c->p, &c->d_misc->best_key, c->stream));
-    c->st_launches++;
-    unsigned long long key = ~0ull;
-    CK(cudaMemcpyAsync(&key, &c->d_misc->best_key, sizeof(key), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
-    ((RecHdr *)c->local_rec.data())->valid = 0;
-    return refresh_local_best(c, key);
+    unsigned long long key;
+    int rc = device_best_key(c, &key);
+    if (rc != FG_OK) return rc;
+    return refresh_local_best(c, key, true);
 }
 
 }  // namespace
@@ -362,6 +398,17 @@ int fg_create(int m, int n, int p, int ring, int r_cap, int64_t num_walkers, int
     alloc((void **)&c->d_pool, words * 8);
     if (rc == FG_OK && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
                         cudaEventCreate(&c->ev2) != cudaSuccess))
+        rc = FG_E_CUDA;
+    if (rc != FG_OK) {
+        cudaGetLastError();
+        fg_destroy(c);
+        return rc;
+    }
+    // unseeded walkers read as rank 0 with zero planes; the best key skips them
+    if (rc == FG_OK && (cudaMemset(c->d_hdr, 0, sizeof(fg_whdr) * num_walkers) != cudaSuccess ||
+                        cudaMemset(c->d_cur, 0, words * num_walkers * 8) != cudaSuccess ||
+                        cudaMemset(c->d_best, 0, words * num_walkers * 8) != cudaSuccess ||
+                        cudaDeviceSynchronize() != cudaSuccess))
         rc = FG_E_CUDA;
     if (rc != FG_OK) {
         cudaGetLastError();
@@ -450,7 +497,7 @@ int fg_load_walkers(fg_ctx *c, const int8_t *coeffs, const int32_t *ranks, int64
     CK(cudaMemcpyAsync(c->d_best + w_begin * words, planes.data(), words * count * 8, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_hdr + w_begin, hdr.data(), sizeof(fg_whdr) * count, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (w_begin == 0 && count == c->W) c->seeded = true;
+    mark_covered(c, w_begin, w_begin + count);
     if (!c->seeded) return FG_OK;
     return recompute_local_best(c);
 }
@@ -529,15 +576,21 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         CK(cudaStreamSynchronize(c->stream));
         verified += hm.restarted;
     }
-    int rc = refresh_local_best(c, hm.best_key);
-    if (rc != FG_OK) return rc;
+    // a walker whose strict improvement failed the Brent check never supplies the
+    // local best (R19): the key is recomputed without the failing walkers
+    unsigned long long key = hm.best_key;
+    if (hm.verify_fail) {
+        int rk = device_best_key(c, &key);
+        if (rk != FG_OK) return rk;
+    }
+    int rc = refresh_local_best(c, key, false);
     c->st_vfail += hm.verify_fail;
     c->st_overflow += hm.q_overflow;
     c->st_steps += steps * (uint64_t)c->W;
     c->st_verified += verified;
     c->st_walk_us += (uint64_t)(walk_ms * 1000.0);
     c->st_verify_us += (uint64_t)(ver_ms * 1000.0);
-    return FG_OK;
+    return rc;
 }
 
 int fg_verify(int m, int n, int p, int ring, const int8_t *coeffs, int rank, int32_t first_fail[3])
@@ -819,6 +872,7 @@ int fg_load_state(fg_ctx *c, const void *buf)
     CK(cudaMemcpyAsync(c->d_cur, pc, words * 8 * c->W, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_best, pc + words * 8 * c->W, words * 8 * c->W, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    c->covered.assign(1, {0, c->W});
     c->seeded = true;
     return recompute_local_best(c);
 }

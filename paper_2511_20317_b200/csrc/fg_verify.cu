@@ -138,7 +138,8 @@ __global__ void restart_kernel(uint64_t *cur, uint64_t *best, fg_whdr *hdr, int6
 }
 
 // R20/R21 local best key over all walkers' best schemes (after seeding / restart /
-// state load; the walk kernel computes the same key in its epilogue)
+// state load, and after a walk in which a verification failed; the walk kernels
+// compute the same key in their epilogue)
 __global__ void bestkey_kernel(const uint64_t *best, const fg_whdr *hdr, int64_t nwalk, int R, int mp,
                                unsigned long long *key)
 {
@@ -146,6 +147,9 @@ __global__ void bestkey_kernel(const uint64_t *best, const fg_whdr *hdr, int64_t
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nwalk; w += nw) {
         const int br = hdr[w].best_r;
+        // unseeded walkers (rank 0) and walkers with a failed Brent check (R19) never
+        // supply the best (whole warp takes the same branch)
+        if (br < 1 || hdr[w].cnt[FG_CNT_VERIFY_FAIL] != 0) continue;
         const uint64_t *b = best + (size_t)w * FG_PLANES * R;
         int nnz = 0;
         for (int l = lane; l < br; l += 32)

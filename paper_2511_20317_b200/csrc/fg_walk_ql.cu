@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         __threadfence();
     }
     const uint64_t done_steps = (uint64_t)chunk * a.chunk_steps;
-    const uint64_t left = a.steps - done_steps;
+    const uint64_t left = done_steps >= a.steps ? 0 : a.steps - done_steps;
     const uint32_t nsteps_task = (uint32_t)(left < a.chunk_steps ? left : a.chunk_steps);
     const int64_t wk_raw = grp * 8 + (lane >> 2);
     // a quad past the last walker stays in the warp (r = 0, no stores)
@@ -817,6 +817,7 @@ cudaError_t launch_ql(const WalkArgs &a, int num_sms, cudaStream_t st)
         const long k = strtol(ev, nullptr, 10);
         if (k >= 1 && k <= 64) b.chunks = (uint32_t)k;
     }
+    if ((uint64_t)b.chunks > a.steps) b.chunks = a.steps > 0 ? (uint32_t)a.steps : 1u;
     b.chunk_steps = (a.steps + b.chunks - 1) / b.chunks;
     const int64_t blocks = groups < resident ? groups : resident;
     walk_ql<P, NWD><<<(unsigned)blocks, QL_THREADS, smem, st>>>(b);

@@ -29,6 +29,14 @@ def _r_cap(rank: int, fmt) -> int:
     return 512
 
 
+def scheme_additions(fmt, ring, coeffs) -> int:
+    """Naive additions of a scheme, computed by libfg (fg_record_pack)."""
+    c = np.asarray(coeffs, dtype=np.int8)
+    r_cap = max(1, c.shape[0])
+    rec = fg.fg_record_pack(*fmt, ring, r_cap, c, 0)
+    return int(fg.fg_record_unpack(rec, r_cap)["additions"])
+
+
 @dataclass
 class Registry:
     """Best scheme per format: lexicographic (rank, additions)."""
@@ -58,7 +66,7 @@ class Explorer:
             rc, _ = fg.fg_verify(*f, ring, c)
             if rc != 0:
                 raise ValueError(f"seed scheme {f} does not verify")
-            self.registry.offer(f, len(c), 0, c)
+            self.registry.offer(f, len(c), scheme_additions(f, ring, c), c)
 
     def walk(self, steps: int):
         """Walk every walker `steps` Alg. 1 iterations, grouped by format."""

@@ -94,3 +94,18 @@ def test_records_pack_merge_unpack(fg, orc):
     assert np.array_equal(u["coeffs"], strassen)
     u0 = fg.fg_record_unpack(recs[0], R)
     assert (u0["rank"], u0["additions"]) == (8, orc.additions(2, 2, 2, naive))
+
+
+def test_explorer_registers_seed_additions(fg, orc):
+    """the exploratory registry starts from each seed's true naive
+    additions, so an equal-rank walk result with fewer additions can
+    replace it."""
+    from paper_2511_20317_b200.explore import Explorer
+    m, n, p, c = load_scheme("scheme_2x2x3_r11.txt")
+    pop = [((2, 2, 2), orc.naive(2, 2, 2)), ((m, n, p), c)]
+    ex = Explorer(pop)
+    assert ex.registry.best[(2, 2, 2)][1] == orc.additions(2, 2, 2, orc.naive(2, 2, 2)) == 4
+    assert ex.registry.best[(m, n, p)][1] == orc.additions(m, n, p, c)
+    r, adds, _ = ex.registry.best[(2, 2, 2)]
+    ex.registry.offer((2, 2, 2), r, adds - 1, orc.naive(2, 2, 2))
+    assert ex.registry.best[(2, 2, 2)][1] == adds - 1
