@@ -180,8 +180,9 @@ int fg_restart(fg_ctx *ctx, int slack, int64_t *restarted);
 
 /* Checkpoint / resume and host-buffer I/O: the complete walker state (planes of
    current and best schemes, ranks, step indices, digests, counters) as an opaque
-   byte image of fg_state_bytes(ctx) bytes.  Resuming from it continues every
-   trajectory bit-exactly (R8). */
+   byte image of fg_state_bytes(ctx) bytes (64-byte header, walker headers, current
+   and best planes, and for the linked-class kernel walk_wl its per-walker class
+   image).  Resuming from it continues every trajectory bit-exactly (R8). */
 size_t fg_state_bytes(const fg_ctx *ctx);
 int fg_save_state(const fg_ctx *ctx, void *host_buf);
 int fg_load_state(fg_ctx *ctx, const void *host_buf);
@@ -255,6 +256,14 @@ int fg_type_invariant(int m, int n, int p, int ring, const int8_t *coeffs, int r
 /* Canonical 64-bit key of a scheme up to row order and per-row sign normalisation
    (PAPER:429): for pool de-duplication.  Host only. */
 int fg_scheme_key(int m, int n, int p, int ring, const int8_t *coeffs, int rank, uint64_t *key);
+
+/* Exact time-to-rank: out[k] (k = 0..max_rank) = the smallest
+   walker step index (0-based Alg. 1 iteration since seeding, R8) in which some walker
+   of this ctx made a VERIFIED strict improvement to rank k (R19), 0 for the seeded
+   rank, UINT64_MAX if rank k was never reached that way.  A strict improvement whose
+   verify-queue entry overflowed is not recorded (fg_stats [7] counts overflows).
+   The box time to rank <= t is then min over k <= t.  FG_E_STATE before seeding. */
+int fg_rank_first_steps(const fg_ctx *ctx, int max_rank, uint64_t *out);
 
 /* Which kernel variant fg_walk uses for this ctx ("warp32_zt_u32k", ...). */
 const char *fg_kernel_name(const fg_ctx *ctx);

@@ -52,6 +52,9 @@ struct fg_ctx {
     DevMisc *d_misc;
     uint32_t *d_task_done;   // walk_ql chunk flags, one per walker group of 8
     uint32_t *d_ql_img;      // walk_ql: shared-memory image per walker between chunks
+    uint32_t *d_wl_img;      // walk_wl: class image per walker between launches
+    unsigned long long *d_rank_first;   // [FG_MAX_RCAP + 1]: first step of a verified improvement to each rank
+    bool img_valid;          // d_wl_img matches the walkers' rows (cleared by every host write)
     uint32_t qcap;
     cudaEvent_t ev0, ev1, ev2;
     // host bests
@@ -229,6 +232,16 @@ int replicate(fg_ctx *c, uint64_t *dst, const uint64_t *src_dev, int64_t words, 
 int recompute_local_best(fg_ctx *c);
 int refresh_local_best(fg_ctx *c, unsigned long long key, bool reset);
 
+// time-to-rank table: nothing reached yet except the seeded rank, at step 0
+int reset_rank_first(fg_ctx *c, int seeded_rank)
+{
+    std::vector<unsigned long long> v(FG_MAX_RCAP + 1, ~0ull);
+    if (seeded_rank >= 0 && seeded_rank <= FG_MAX_RCAP) v[seeded_rank] = 0;
+    CK(cudaMemcpyAsync(c->d_rank_first, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return FG_OK;
+}
+
 // record [w0, w1) as seeded; the ctx is walkable once the ranges cover [0, W)
 void mark_covered(fg_ctx *c, int64_t w0, int64_t w1)
 {
@@ -270,6 +283,11 @@ int seed_planes(fg_ctx *c, const uint64_t *planes, int rank, int64_t w0, int64_t
     CK(cudaStreamSynchronize(c->stream));
     if (rc != FG_OK) return rc;
     mark_covered(c, w0, w1);
+    c->img_valid = false;
+    if (c->seeded) {
+        int rr = reset_rank_first(c, rank);
+        if (rr != FG_OK) return rr;
+    }
     // the local best is defined once every walker holds a scheme (a partial
     // seed must not let zeroed headers of unseeded walkers into the best key)
     return c->seeded ? recompute_local_best(c) : FG_OK;
@@ -395,7 +413,9 @@ int fg_create(int m, int n, int p, int ring, int r_cap, int64_t num_walkers, int
     alloc((void **)&c->d_task_done, sizeof(uint32_t) * (size_t)((num_walkers + 7) / 8 + 1));
     if (kind == FG_K_QL_P16 || kind == FG_K_QL_Z2)   // 6 R + R / 4 slots + 5 scalars, R <= 128
         alloc((void **)&c->d_ql_img, sizeof(uint32_t) * (size_t)(6 * 128 + 32 + 5) * num_walkers);
+    if (fg_kind_is_wl(kind)) alloc((void **)&c->d_wl_img, sizeof(uint32_t) * fg_wl_img_words(r_cap) * num_walkers);
     alloc((void **)&c->d_pool, words * 8);
+    alloc((void **)&c->d_rank_first, sizeof(unsigned long long) * (FG_MAX_RCAP + 1));
     if (rc == FG_OK && (cudaEventCreate(&c->ev0) != cudaSuccess || cudaEventCreate(&c->ev1) != cudaSuccess ||
                         cudaEventCreate(&c->ev2) != cudaSuccess))
         rc = FG_E_CUDA;
@@ -427,6 +447,7 @@ void fg_destroy(fg_ctx *c)
     cudaSetDevice(c->device);
     cudaFree(c->d_cur); cudaFree(c->d_best); cudaFree(c->d_hdr); cudaFree(c->d_qplanes);
     cudaFree(c->d_qmeta); cudaFree(c->d_misc); cudaFree(c->d_pool); cudaFree(c->d_task_done); cudaFree(c->d_ql_img);
+    cudaFree(c->d_wl_img); cudaFree(c->d_rank_first);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev2) cudaEventDestroy(c->ev2);
@@ -498,6 +519,13 @@ int fg_load_walkers(fg_ctx *c, const int8_t *coeffs, const int32_t *ranks, int64
     CK(cudaMemcpyAsync(c->d_hdr + w_begin, hdr.data(), sizeof(fg_whdr) * count, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     mark_covered(c, w_begin, w_begin + count);
+    c->img_valid = false;
+    if (c->seeded) {
+        int rmin = FG_MAX_RCAP;
+        for (int64_t k = 0; k < count; ++k) rmin = std::min(rmin, (int)ranks[k]);
+        int rr = reset_rank_first(c, rmin);
+        if (rr != FG_OK) return rr;
+    }
     if (!c->seeded) return FG_OK;
     return recompute_local_best(c);
 }
@@ -526,6 +554,10 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.work_counter = &c->d_misc->work_counter;
     a.task_done = c->d_task_done;
     a.ql_img = c->d_ql_img;
+    a.wl_img = c->d_wl_img;
+    // the complexity mode (R24) runs the round-1 kernels; walk_wl's layouts map to walk_wm
+    int kind = c->kind;
+    if (a.mode) kind = fg_kind_is_wl(kind) ? fg_multi_kind(c->ring, c->maxlen, c->R) : fg_kind_for_mode(kind);
     a.dbg = getenv("FG_DBG") ? (uint32_t)strtoul(getenv("FG_DBG"), nullptr, 0) : 0u;
     a.dbgbuf = c->d_misc->dbgbuf;
     VerifyArgs v;
@@ -547,10 +579,16 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         CK(cudaMemsetAsync(&c->d_misc->work_counter, 0, sizeof(unsigned long long), c->stream));
         CK(cudaMemsetAsync(c->d_task_done, 0, sizeof(uint32_t) * (size_t)((c->W + 7) / 8 + 1), c->stream));
         CK(cudaEventRecord(c->ev0, c->stream));
-        CK(fg_launch_walk(a.mode ? fg_kind_for_mode(c->kind) : c->kind, a, c->num_sms, c->stream));
+        a.img_valid = c->img_valid ? 1u : 0u;
+        CK(fg_launch_walk(kind, a, c->num_sms, c->stream));
+        c->img_valid = fg_kind_is_wl(kind);
         CK(cudaEventRecord(c->ev1, c->stream));
         CK(fg_launch_verify(v, c->stream));
         CK(cudaEventRecord(c->ev2, c->stream));
+        if (a.mode == 0) {
+            CK(fg_launch_rank_first(c->d_qmeta, &c->d_misc->q_count, c->qcap, c->d_rank_first, c->stream));
+            c->st_launches++;
+        }
         c->st_launches += 2;
         c->st_walk_launches++;
         CK(cudaMemcpyAsync(&hm, c->d_misc, sizeof(hm), cudaMemcpyDeviceToHost, c->stream));
@@ -823,6 +861,7 @@ int fg_restart(fg_ctx *c, int slack, int64_t *restarted)
     CK(cudaMemsetAsync(&c->d_misc->restarted, 0, sizeof(unsigned long long), c->stream));
     CK(fg_launch_restart(c->d_cur, c->d_best, c->d_hdr, c->W, c->R, c->d_pool, b->rank, b->additions, slack,
                          &c->d_misc->restarted, c->stream));
+    c->img_valid = false;
     c->st_launches++;
     unsigned long long n = 0;
     CK(cudaMemcpyAsync(&n, &c->d_misc->restarted, sizeof(n), cudaMemcpyDeviceToHost, c->stream));
@@ -831,11 +870,18 @@ int fg_restart(fg_ctx *c, int slack, int64_t *restarted)
     return recompute_local_best(c);
 }
 
+// walk_wl's class image travels with the state (a checkpoint resumes without rebuilding
+// the class lists); other kernels have none
+static size_t img_bytes(const fg_ctx *c)
+{
+    return c->d_wl_img ? fg_wl_img_words(c->R) * 4 * (size_t)c->W : 0;
+}
+
 size_t fg_state_bytes(const fg_ctx *c)
 {
     if (!c) return 0;
     const size_t words = (size_t)FG_PLANES * c->R;
-    return 64 + sizeof(fg_whdr) * c->W + 2 * words * 8 * c->W;
+    return 64 + sizeof(fg_whdr) * c->W + 2 * words * 8 * c->W + img_bytes(c);
 }
 
 int fg_save_state(const fg_ctx *c, void *buf)
@@ -845,13 +891,16 @@ int fg_save_state(const fg_ctx *c, void *buf)
     CK(cudaSetDevice(c->device));
     const size_t words = (size_t)FG_PLANES * c->R;
     unsigned char *b = (unsigned char *)buf;
+    const size_t ib = img_bytes(c);
     uint32_t hdr[16] = {STATE_MAGIC, (uint32_t)c->m, (uint32_t)c->n, (uint32_t)c->p, (uint32_t)c->ring,
-                        (uint32_t)c->R, (uint32_t)(c->W & 0xffffffff), (uint32_t)(c->W >> 32)};
+                        (uint32_t)c->R, (uint32_t)(c->W & 0xffffffff), (uint32_t)(c->W >> 32),
+                        (uint32_t)(ib ? fg_wl_img_words(c->R) : 0), (uint32_t)(ib && c->img_valid)};
     memcpy(b, hdr, 64);
     CK(cudaMemcpyAsync(b + 64, c->d_hdr, sizeof(fg_whdr) * c->W, cudaMemcpyDeviceToHost, c->stream));
     unsigned char *pc = b + 64 + sizeof(fg_whdr) * c->W;
     CK(cudaMemcpyAsync(pc, c->d_cur, words * 8 * c->W, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(pc + words * 8 * c->W, c->d_best, words * 8 * c->W, cudaMemcpyDeviceToHost, c->stream));
+    if (ib) CK(cudaMemcpyAsync(pc + 2 * words * 8 * c->W, c->d_wl_img, ib, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return FG_OK;
 }
@@ -871,8 +920,13 @@ int fg_load_state(fg_ctx *c, const void *buf)
     const unsigned char *pc = b + 64 + sizeof(fg_whdr) * c->W;
     CK(cudaMemcpyAsync(c->d_cur, pc, words * 8 * c->W, cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->d_best, pc + words * 8 * c->W, words * 8 * c->W, cudaMemcpyHostToDevice, c->stream));
+    // a class image saved by the same kind of context resumes as it was saved
+    const size_t ib = img_bytes(c);
+    const bool img = ib && hdr[8] == (uint32_t)fg_wl_img_words(c->R) && hdr[9] == 1u;
+    if (img) CK(cudaMemcpyAsync(c->d_wl_img, pc + 2 * words * 8 * c->W, ib, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->covered.assign(1, {0, c->W});
+    c->img_valid = img;
     c->seeded = true;
     return recompute_local_best(c);
 }
@@ -901,6 +955,18 @@ int fg_stats(const fg_ctx *c, uint64_t out[12])
     out[9] = c->st_walk_us;
     out[10] = c->st_verify_us;
     out[11] = c->st_walk_launches;
+    return FG_OK;
+}
+
+int fg_rank_first_steps(const fg_ctx *c, int max_rank, uint64_t *out)
+{
+    if (!c || !out || max_rank < 0) return FG_E_ARG;
+    if (!c->seeded) return FG_E_STATE;
+    CK(cudaSetDevice(c->device));
+    std::vector<unsigned long long> v(FG_MAX_RCAP + 1);
+    CK(cudaMemcpyAsync(v.data(), c->d_rank_first, v.size() * sizeof(v[0]), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    for (int k = 0; k <= max_rank; ++k) out[k] = k <= FG_MAX_RCAP ? (uint64_t)v[k] : ~0ull;
     return FG_OK;
 }
 

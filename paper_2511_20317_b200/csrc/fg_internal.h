@@ -62,6 +62,8 @@ struct WalkArgs {
     uint32_t chunks;                    // walk_ql: step chunks per group (set by its launcher)
     uint64_t chunk_steps;
     uint32_t *ql_img;                   // walk_ql: per-walker shared-memory image between chunks
+    uint32_t *wl_img;                   // walk_wl: per-walker class image (links, later counts) between launches
+    uint32_t img_valid;                 // walk_wl: wl_img matches the walkers' current rows
     uint32_t mode;                      // 0 = Alg. 1 walk, 1 = naive-complexity minimisation (R24)
     uint32_t dbg;                       // debug switches (env FG_DBG), 0 in production
     uint32_t *dbgbuf;                   // 16 words of debug output (first error wins)
@@ -81,7 +83,11 @@ struct VerifyArgs {
 // launchers (fg_walk.cu / fg_verify.cu); return cudaError_t
 enum fg_kernel_kind { FG_K_NONE = 0, FG_K_W32_ZT_K16, FG_K_W32_ZT_K32, FG_K_W32_Z2_K32,
                       FG_K_WM_P16, FG_K_WM_P32, FG_K_WM_P64, FG_K_WM_Z2, FG_K_WM_Z64,
-                      FG_K_H16_P16, FG_K_H16_P32, FG_K_H16_Z2, FG_K_T1_P16, FG_K_T1_Z2, FG_K_Q4_P16, FG_K_Q4_Z2, FG_K_QL_P16, FG_K_QL_Z2 };
+                      FG_K_H16_P16, FG_K_H16_P32, FG_K_H16_Z2, FG_K_T1_P16, FG_K_T1_Z2, FG_K_Q4_P16, FG_K_Q4_Z2, FG_K_QL_P16, FG_K_QL_Z2,
+                      FG_K_WL_P16, FG_K_WL_P32, FG_K_WL_P64, FG_K_WL_Z2, FG_K_WL_Z64 };
+cudaError_t fg_launch_walk_wl(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
+size_t fg_wl_img_words(int R);     // walk_wl class image words per walker
+bool fg_kind_is_wl(int kind);
 cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, cudaStream_t st);
 cudaError_t fg_launch_walk_t1(int kind, const WalkArgs &a, cudaStream_t st);
@@ -100,5 +106,7 @@ int fg_kind_for_mode(int kind);
 cudaError_t fg_launch_verify_flagged(const uint64_t *best, fg_whdr *hdr, int64_t num_walkers, int R, int m,
                                      int n, int p, int ring, uint32_t *fail_count, unsigned long long *done,
                                      cudaStream_t st);   // R24 runs on the quad, one-walker-per-warp and multi-row kernels
+cudaError_t fg_launch_rank_first(const fg_qmeta *meta, const uint32_t *count_ptr, uint32_t cap,
+                                 unsigned long long *first, cudaStream_t st);
 cudaError_t fg_launch_bestkey(const uint64_t *best, const fg_whdr *hdr, int64_t num_walkers, int R, int mp,
                               unsigned long long *key, cudaStream_t st);

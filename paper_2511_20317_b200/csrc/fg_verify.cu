@@ -164,7 +164,25 @@ __global__ void bestkey_kernel(const uint64_t *best, const fg_whdr *hdr, int64_t
     }
 }
 
+// Exact time-to-rank: the first step index at which a VERIFIED strict
+// improvement reached each rank, from the verify queue entries of this launch.
+__global__ void rank_first_kernel(const fg_qmeta *meta, const uint32_t *count_ptr, uint32_t cap,
+                                  unsigned long long *first)
+{
+    const uint32_t count = min(*count_ptr, cap);
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < count; q += gridDim.x * blockDim.x)
+        if (meta[q].ok == 1 && meta[q].rank >= 0 && meta[q].rank <= FG_MAX_RCAP)
+            atomicMin(first + meta[q].rank, (unsigned long long)meta[q].step);
+}
+
 }  // namespace
+
+cudaError_t fg_launch_rank_first(const fg_qmeta *meta, const uint32_t *count_ptr, uint32_t cap,
+                                 unsigned long long *first, cudaStream_t st)
+{
+    rank_first_kernel<<<64, 256, 0, st>>>(meta, count_ptr, cap, first);
+    return cudaGetLastError();
+}
 
 cudaError_t fg_launch_bestkey(const uint64_t *best, const fg_whdr *hdr, int64_t num_walkers, int R, int mp,
                               unsigned long long *key, cudaStream_t st)

@@ -599,13 +599,20 @@ int fg_pick_kernel(int ring, int maxlen, int R)
     // 33 <= R <= 128, one-word factors: the linked-class quad kernel (fg_walk_ql.cu),
     // faster than walk_wm on (4,4,4) Z_T and Z_2 (profiles/r01_bench_multi.txt);
     // FG_WALK_KERNEL=wm forces the one-walker-per-warp multi-row kernel.
+    // Everything else with 33 <= R <= 512 (wide factors or R > 128: configs C4, C5) runs
+    // the linked-class one-walker-per-warp kernel (fg_walk_wl.cuh);
+    // FG_WALK_KERNEL=wm forces the round-1 multi-row kernel, =wl forces walk_wl also
+    // where walk_ql is the default.
     const char *env = getenv("FG_WALK_KERNEL");
     const bool wm = env && strcmp(env, "wm") == 0;
-    if (R <= 128 && !wm) {
+    const bool wl = env && strcmp(env, "wl") == 0;
+    if (R <= 128 && !wm && !wl) {
         if (ring == FG_ZT && maxlen <= 16) return FG_K_QL_P16;
         if (ring == FG_Z2 && maxlen <= 32) return FG_K_QL_Z2;
     }
-    return fg_multi_kind(ring, maxlen, R);
+    if (wm || R > 512) return fg_multi_kind(ring, maxlen, R);
+    if (ring == FG_ZT) return maxlen <= 16 ? FG_K_WL_P16 : (maxlen <= 32 ? FG_K_WL_P32 : FG_K_WL_P64);
+    return maxlen <= 32 ? FG_K_WL_Z2 : FG_K_WL_Z64;
 }
 
 int fg_kind_for_mode(int kind)
@@ -642,6 +649,11 @@ const char *fg_kernel_kind_name(int kind)
     case FG_K_Q4_Z2: return "walk_q4<PZ2>";
     case FG_K_QL_P16: return "walk_ql<P16>";
     case FG_K_QL_Z2: return "walk_ql<PZ2>";
+    case FG_K_WL_P16: return "walk_wl<P16>";
+    case FG_K_WL_P32: return "walk_wl<P32>";
+    case FG_K_WL_P64: return "walk_wl<P64>";
+    case FG_K_WL_Z2: return "walk_wl<PZ2>";
+    case FG_K_WL_Z64: return "walk_wl<PZ64>";
     default: return "none";
     }
 }
@@ -661,6 +673,11 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_Q4_Z2: return fg_launch_walk_q4(kind, a, st);
     case FG_K_QL_P16:
     case FG_K_QL_Z2: return fg_launch_walk_ql(kind, a, num_sms, st);
+    case FG_K_WL_P16:
+    case FG_K_WL_P32:
+    case FG_K_WL_P64:
+    case FG_K_WL_Z2:
+    case FG_K_WL_Z64: return fg_launch_walk_wl(kind, a, num_sms, st);
     default: return fg_launch_walk_multi(kind, fg_multi_ns(a.R), a, num_sms, st);
     }
 }

@@ -70,6 +70,7 @@ _sig = {
     "fg_load_state": (_i32, [_vp, _vp]),
     "fg_stats": (_i32, [_vp, _vp]),
     "fg_kernel_name": (C.c_char_p, [_vp]),
+    "fg_rank_first_steps": (_i32, [_vp, _i32, _vp]),
     "fg_meta_transpose": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
     "fg_meta_rotate": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
     "fg_meta_swap_sizes": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
@@ -364,6 +365,14 @@ class FlipGraph:
 
     def load_state(self, buf):
         _ck(_lib.fg_load_state(self.ctx, _p(buf)), "fg_load_state")
+
+    def rank_first_steps(self, max_rank=None) -> np.ndarray:
+        """out[k]: first walker step index of a verified strict improvement to rank k
+        (0 for the seeded rank, 2^64-1 if never reached)."""
+        max_rank = self.R if max_rank is None else max_rank
+        out = np.zeros(max_rank + 1, np.uint64)
+        _ck(_lib.fg_rank_first_steps(self.ctx, max_rank, _p(out)), "fg_rank_first_steps")
+        return out
 
     def stats(self) -> dict:
         out = np.zeros(12, np.uint64)

@@ -182,7 +182,7 @@ def _state_views(buf, W, R):
     hdr = buf[64: 64 + HDR * W].reshape(W, HDR)
     words = 6 * R * 8
     cur = buf[64 + HDR * W: 64 + HDR * W + words * W].reshape(W, words)
-    best = buf[64 + HDR * W + words * W:].reshape(W, words)
+    best = buf[64 + HDR * W + words * W: 64 + HDR * W + 2 * words * W].reshape(W, words)
     return hdr, cur, best
 
 

@@ -134,3 +134,60 @@ def test_fuzz_ql(fg, orc, idx):
     ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed, params=OracleParams.default(**prm))
     for k in ("r", "best_r", "digest", "cnt", "rows", "best"):
         assert np.array_equal(got[k], ref[k]), f"ql config {idx} {QL_CONFIGS[idx]}: {k} differs"
+
+
+def _wide_configs(n=10, seed=4242):
+    """Formats with two-word factors (Z_T > 16 or Z_2 > 32 elements) or R > 128: the
+    walk_wl (default) / walk_wm layouts.  Some walker counts exceed the resident warps,
+    so the persistent walker queue hands several walkers to one warp."""
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        m, nn, p = (int(x) for x in rng.integers(2, 8, size=3))
+        ring = int(rng.integers(0, 2))
+        naive = m * nn * p
+        maxlen = max(m * nn, nn * p, p * m)
+        if maxlen > 64 or naive + 4 > 512 or naive > 260:
+            continue
+        wide = maxlen > (16 if ring == 0 else 32) or naive + 8 > 128
+        if not wide:
+            continue
+        R = int(min(512, naive + int(rng.integers(4, 40))))
+        prm = dict(k_flip=int(rng.integers(1, 17)), thr_accept_eq=int(rng.integers(0, 1 << 31)),
+                   thr_reduce=int(rng.integers(0, 1 << 32)), thr_expand=int(rng.integers(0, 1 << 29)),
+                   expand_slack=int(rng.integers(-1, 4)))
+        W = int(rng.choice([37, 160, 2600]))
+        steps = int(rng.integers(150, 500))
+        out.append(((m, nn, p), ring, R, prm, W, steps, int(rng.integers(1, 1 << 62))))
+    return out
+
+
+WIDE_CONFIGS = _wide_configs()
+
+
+@pytest.mark.parametrize("kernel", ["wl", "wm"])
+@pytest.mark.parametrize("idx", range(len(WIDE_CONFIGS)))
+def test_fuzz_wide(fg, orc, kernel, idx):
+    import torch
+    from paper_2511_20317_b200.inputs import sample_walkers
+    (m, n, p), ring, R, prm, W, steps, seed = WIDE_CONFIGS[idx]
+    old = os.environ.get("FG_WALK_KERNEL")
+    os.environ["FG_WALK_KERNEL"] = kernel
+    try:
+        g = fg.FlipGraph(m, n, p, ring, R, W, 0, 0, torch.cuda.current_stream().cuda_stream)
+    finally:
+        if old is None:
+            del os.environ["FG_WALK_KERNEL"]
+        else:
+            os.environ["FG_WALK_KERNEL"] = old
+    assert g.kernel_name.startswith("walk_" + kernel), g.kernel_name
+    g.seed_naive()
+    half = steps // 2
+    g.walk(half, seed, fg.params_default(**prm))
+    g.walk(steps - half, seed, fg.params_default(**prm))
+    got = g.get_walkers()
+    ids = sample_walkers(W, 10, seed=idx)
+    ref = orc.run_walkers(m, n, p, ring, R, 0, 0, steps, seed, params=OracleParams.default(**prm), ids=ids)
+    for k in ("r", "best_r", "digest", "cnt", "rows", "best"):
+        assert np.array_equal(got[k][ids], ref[k]), f"wide config {idx} {WIDE_CONFIGS[idx]}: {k} differs"
+    assert g.stats()["verify_fail"] == 0

@@ -16,7 +16,7 @@ from paper_2511_20317_b200.inputs import WORKLOADS, sample_walkers
 pytestmark = pytest.mark.gpu
 ZT, Z2 = 0, 1
 KERNELS = {"w32": "walk_w32", "h16": "walk_h16", "t1": "walk_t1", "q4": "walk_q4"}
-KERNEL_PREFIX = dict(KERNELS, ql="walk_ql", wm="walk_wm")
+KERNEL_PREFIX = dict(KERNELS, ql="walk_ql", wm="walk_wm", wl="walk_wl")
 
 
 @pytest.fixture(scope="module")
@@ -172,3 +172,37 @@ def test_ql_chunked_tasks(fg, orc):
     ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, 0xC4C4)
     _check(got, ref, None)
     assert np.all(got["step"] == steps)
+
+
+@pytest.mark.parametrize("case", [((4, 4, 4), ZT, 96, 61, 2000), ((3, 3, 3), ZT, 33, 45, 3000), ((3, 4, 4), ZT, 64, 29, 2500),
+                                  ((4, 4, 4), Z2, 96, 40, 2000), ((3, 3, 3), Z2, 64, 45, 2500)],
+                         ids=lambda c: f"{c[0]}-{'zt' if c[1] == ZT else 'z2'}-R{c[2]}")
+def test_wl_forced_for_one_word(fg, orc, case):
+    """The linked-class one-walker-per-warp kernel (default for wide factors and R > 128)
+    on one-word formats through FG_WALK_KERNEL=wl, every walker, across two launches
+    (the second resumes from the class image)."""
+    (m, n, p), ring, R, W, steps = case
+    seed = 0x3B + R
+    g = _ctx(fg, "wl", m, n, p, ring, R, W)
+    g.seed_naive()
+    g.walk(steps, seed, fg.params_default(phase_steps=steps // 3 + 1))
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
+    _check(got, ref, None)
+
+
+@pytest.mark.parametrize("case", [((5, 5, 5), ZT, 160, 96, 600), ((4, 5, 12), ZT, 256, 40, 300),
+                                  ((4, 5, 12), Z2, 256, 40, 300), ((4, 4, 4), Z2, 160, 64, 800)],
+                         ids=lambda c: f"{c[0]}-{'zt' if c[1] == ZT else 'z2'}-R{c[2]}")
+def test_wm_forced_for_wide(fg, orc, case):
+    """The round-1 multi-row kernel stays covered on the C4 / C5 layouts (P32, P64, PZ64,
+    PZ2 with R > 128) through FG_WALK_KERNEL=wm."""
+    (m, n, p), ring, R, W, steps = case
+    seed = 0x3C + R
+    g = _ctx(fg, "wm", m, n, p, ring, R, W)
+    g.seed_naive()
+    g.walk(steps, seed)
+    got = g.get_walkers()
+    ids = sample_walkers(W, 8, seed=R)
+    ref = orc.run_walkers(m, n, p, ring, R, 0, 0, steps, seed, ids=ids)
+    _check(got, ref, ids)

@@ -236,7 +236,7 @@ def test_multi_row_kernel_parity(fg, orc, case):
     g = _ctx(fg, m, n, p, ring, R, W, base=77)
     # one-word factors with R <= 128 run on the linked-class quad kernel (walk_ql)
     maxlen = max(m * n, n * p, p * m)
-    assert g.kernel_name.startswith("walk_ql" if R <= 128 and maxlen <= (16 if ring == ZT else 32) else "walk_wm")
+    assert g.kernel_name.startswith("walk_ql" if R <= 128 and maxlen <= (16 if ring == ZT else 32) else "walk_wl")
     g.seed_naive()
     seed = 0x2511203170000000 + 2 + ring
     half = steps // 2
