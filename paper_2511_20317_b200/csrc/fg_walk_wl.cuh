@@ -9,12 +9,14 @@
 // per warp, which does not fit shared memory for R >= 160 two-word factors.  Here one
 // walker per warp keeps, per row l (lane l % 32, word l / 32):
 //   fac[X][l]  factor X (U and V sign-normalised; W up to sign)
-//   nx[l]      the next row of l's U / V / W class (10 bits each; 1023 = none) and,
-//              in bit 30, the sign of w (the stored W key is the positive form)
+//   nxh[X][l]  the next row of l's class in role X (1023 = none)
+//   wsb        the signs of the w factors, one bit per row (the stored W key is the
+//              positive form, W classes are "equal up to sign")
 //   lc[l]      later counts of the three classes, 10 bits each (R10)
-//   tw[w]      per 32-row word the sum of its rows' later counts (U | V << 16, W)
-// so a draw (R11) is two warp scans (word totals, then the word's later counts) and
-// `hops` next-pointer steps, and a flip commit is ONE compare pass over the rows
+//   tw[w]      per 32-row word the sum of its rows' later counts (U | V << 16; W)
+// so a draw (R11) is a lookup in the per-step prefix of the word totals, one warp scan
+// of the word's later counts and `hops` next-pointer steps, and a flip commit is ONE
+// compare pass over the rows
 // for both changed factors (they are in different roles, so the two class updates
 // commute) that also gives R12's exact skip test (does a touched row share two
 // factors with another row?), as in walk_ql.  The class structure (nx, lc, tw and the
@@ -29,12 +31,11 @@ namespace fgwl {
 using namespace fgd;
 
 constexpr int NIL = 1023;
-constexpr uint32_t NIL3 = 0x3FFFFFFFu;          // three empty next fields
-constexpr uint32_t WSIGN = 1u << 30;
 constexpr int PXS = 9;                         // Philox table stride (32 steps x 9 words)
 constexpr int IMG_SCALARS = 8;                 // nCU, nCV, nCW, dset lo, dset hi, nD, dover, r
 
-__host__ __device__ constexpr int img_words(int nwd) { return 2 * 32 * nwd + 2 * nwd + IMG_SCALARS; }
+// class image per walker (HBM): nxh (3 RM u16), lc (RM), tw (32), wsb (16), scalars
+__host__ __device__ constexpr int img_words(int nwd) { return 48 * nwd + 32 * nwd + 32 + 16 + IMG_SCALARS; }
 
 __device__ __forceinline__ uint32_t below_in(int l, int w)      // bits of word w for rows < l
 {
@@ -55,12 +56,19 @@ __device__ __forceinline__ int getf(uint32_t x, int X) { return (int)((x >> (10 
 // one walker's shared-memory state
 template <class P> struct WS {
     typename P::F *fac;   // [3][RM]
-    uint32_t *nx;         // [RM]
+    uint16_t *nxh;        // [3][RM]
     uint32_t *lc;         // [RM]
-    uint32_t *tw;         // [2][nwd]
+    uint32_t *wsb;        // [16]
+    uint32_t *tw;         // [32]: U | V << 16 at w, W at 16 + w
     int nwd, RM;
     __device__ __forceinline__ typename P::F key(int X, int l) const { return fac[X * RM + l]; }
-    __device__ __forceinline__ uint32_t wsg(int l) const { return (nx[l] >> 30) & 1u; }
+    __device__ __forceinline__ int nxt(int X, int l) const { return (int)nxh[X * RM + l]; }
+    __device__ __forceinline__ void set_nxt(int X, int l, int v) const { nxh[X * RM + l] = (uint16_t)v; }
+    __device__ __forceinline__ uint32_t wsg(int l) const { return (wsb[l >> 5] >> (l & 31)) & 1u; }
+    __device__ __forceinline__ void set_wsg(int l, uint32_t v) const      // lane 0
+    {
+        wsb[l >> 5] = (wsb[l >> 5] & ~(1u << (l & 31))) | ((v & 1u) << (l & 31));
+    }
     __device__ __forceinline__ typename P::F full(int X, int l) const
     {
         const typename P::F k = key(X, l);
@@ -77,7 +85,7 @@ template <class P> struct WS {
     // word total of role X (lane 0 only)
     __device__ __forceinline__ void tw_add(int w, int X, int d) const
     {
-        if (X == 2) tw[nwd + w] += (uint32_t)d;
+        if (X == 2) tw[16 + w] += (uint32_t)d;
         else tw[w] += (uint32_t)d << (16 * X);
     }
 };
@@ -118,9 +126,9 @@ __device__ __noinline__ int key_change(WS<P> s, int r, int t, int X, typename P:
     }
     __syncwarp();
     if (lane == 0) {
-        if (pO != NIL) s.nx[pO] = setf(s.nx[pO], X, sO);
-        if (pK != NIL) s.nx[pK] = setf(s.nx[pK], X, t);
-        s.nx[t] = setf(s.nx[t], X, sK);
+        if (pO != NIL) s.set_nxt(X, pO, sO);
+        if (pK != NIL) s.set_nxt(X, pK, t);
+        s.set_nxt(X, t, sK);
         const int old = getf(s.lc[t], X);
         s.lc[t] = setf(s.lc[t], X, aK);
         s.tw_add(t >> 5, X, aK - old);
@@ -140,7 +148,7 @@ __device__ __noinline__ D3 set_row(WS<P> s, int r, int l, Row<P> nr, bool fresh)
     const int lane = threadIdx.x & 31;
     D3 d = {0, 0, 0};
     if (fresh) {
-        if (lane == 0) { s.nx[l] = NIL3; s.lc[l] = 0u; }
+        if (lane == 0) { s.set_nxt(0, l, NIL); s.set_nxt(1, l, NIL); s.set_nxt(2, l, NIL); s.lc[l] = 0u; }
         __syncwarp();
     }
 #pragma unroll 1
@@ -154,7 +162,7 @@ __device__ __noinline__ D3 set_row(WS<P> s, int r, int l, Row<P> nr, bool fresh)
         d.d1 += X == 1 ? v : 0;
         d.d2 += X == 2 ? v : 0;
     }
-    if (lane == 0) s.nx[l] = (s.nx[l] & ~WSIGN) | (P::first_neg(nr.w) ? WSIGN : 0u);
+    if (lane == 0) s.set_wsg(l, P::first_neg(nr.w) ? 1u : 0u);
     __syncwarp();
     return d;
 }
@@ -212,10 +220,10 @@ __device__ __noinline__ uint32_t check_structure(WS<P> s, int r, uint32_t nCU, u
                     for (int j = l + 1; j < r; ++j)
                         if (P::eq(s.key(X, j), k)) { if (first == NIL) first = j; cnt++; }
                 if (getf(s.lc[l], X) != cnt) bad |= 1u;
-                if (getf(s.nx[l], X) != first) bad |= 2u;
+                if (s.nxt(X, l) != first) bad |= 2u;
             }
             const int sum = __reduce_add_sync(FULL, (uint32_t)cnt);
-            const uint32_t t = X == 2 ? s.tw[s.nwd + w] : ((s.tw[w] >> (16 * X)) & 0xFFFFu);
+            const uint32_t t = X == 2 ? s.tw[16 + w] : ((s.tw[w] >> (16 * X)) & 0xFFFFu);
             if ((uint32_t)sum != t) bad |= 4u;
             tot[X] += (uint32_t)sum;
         }
@@ -232,13 +240,14 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
     const int RM = 32 * nwd;
     WS<P> s;
     s.fac = reinterpret_cast<F *>(smraw);
-    s.nx = reinterpret_cast<uint32_t *>(s.fac + 3 * RM);
-    s.lc = s.nx + RM;
+    s.lc = reinterpret_cast<uint32_t *>(s.fac + 3 * RM);
     s.tw = s.lc + RM;
+    s.wsb = s.tw + 32;
+    uint32_t *px = s.wsb + 16;                                 // Philox table [32][PXS]
+    uint32_t *rc = px + 32 * PXS;                              // 8 rare counters
+    s.nxh = reinterpret_cast<uint16_t *>(rc + 8);
     s.nwd = nwd;
     s.RM = RM;
-    uint32_t *px = s.tw + 2 * 16;                              // Philox table [32][PXS]
-    uint32_t *rc = px + 32 * PXS;                              // 8 rare counters
     const int lane = threadIdx.x;
     const int R = a.R;
     const uint64_t seed = a.seed;
@@ -274,11 +283,13 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
             s.fac[l] = u;
             s.fac[RM + l] = v;
             s.fac[2 * RM + l] = P::abs(w);
-            s.nx[l] = NIL3 | (P::first_neg(w) ? WSIGN : 0u);
+            s.set_nxt(0, l, NIL); s.set_nxt(1, l, NIL); s.set_nxt(2, l, NIL);
             s.lc[l] = 0u;
+            const uint32_t sg = __ballot_sync(FULL, P::first_neg(w));
+            if (lane == 0) s.wsb[l >> 5] = sg;
         }
         if (lane < 8) rc[lane] = 0;
-        if (lane < 2 * 16) s.tw[lane] = 0;
+        s.tw[lane] = 0;
         __syncwarp();
         uint32_t nCU = 0, nCV = 0, nCW = 0;
         // R15 dirty set D (<= 6 rows, 10 bits each): only rows changed by expands since
@@ -289,13 +300,14 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
         uint32_t *img = a.wl_img ? a.wl_img + (size_t)wk * IMGW : nullptr;
         const bool resume = img != nullptr && a.img_valid && (int)img[IMGW - 1] == r;
         if (resume) {
+            const uint32_t *nxi = img, *lci = img + 3 * RM / 2, *twi = lci + RM;
 #pragma unroll 1
-            for (int l = lane; l < RM; l += 32) {
-                s.nx[l] = img[l];
-                s.lc[l] = img[RM + l];
-            }
-            if (lane < 2 * nwd) s.tw[lane] = img[2 * RM + lane];
-            const uint32_t *sc = img + 2 * RM + 2 * nwd;
+            for (int k = lane; k < 3 * RM / 2; k += 32) reinterpret_cast<uint32_t *>(s.nxh)[k] = nxi[k];
+#pragma unroll 1
+            for (int l = lane; l < RM; l += 32) s.lc[l] = lci[l];
+            s.tw[lane] = twi[lane];
+            if (lane < 16) s.wsb[lane] = twi[32 + lane];
+            const uint32_t *sc = twi + 48;
             nCU = sc[0]; nCV = sc[1]; nCW = sc[2];
             dset = (uint64_t)sc[3] | ((uint64_t)sc[4] << 32);
             nD = (int)sc[5];
@@ -316,7 +328,7 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
                                 if (P::eq(s.key(X, j), k)) { if (first == NIL) first = j; cnt++; }
                         }
                     }
-                    s.nx[l] = setf(s.nx[l], X, first);
+                    s.set_nxt(X, l, first);
                     s.lc[l] = setf(s.lc[l], X, cnt);
                     const uint32_t sum = __reduce_add_sync(FULL, (uint32_t)cnt);
                     if (lane == 0) s.tw_add(w, X, (int)sum);
@@ -580,6 +592,20 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
 
             // ---- R11 try_flip: sequential draws over 4|C| (R9) ----
             if (nC) {
+                // prefix of the word totals, once per step (the list is not rebuilt between
+                // draws): lane w holds the inclusive sums of words 0..w, 3 x 21-bit fields
+                uint64_t tv = 0;
+                if (lane < nwd) {
+                    const uint32_t t0 = s.tw[lane], t1 = s.tw[16 + lane];
+                    tv = (uint64_t)(t0 & 0xFFFFu) | ((uint64_t)(t0 >> 16) << 21) | ((uint64_t)t1 << 42);
+                }
+                uint64_t inc = tv;
+#pragma unroll
+                for (int o = 1; o < 16; o <<= 1) {
+                    const uint64_t t = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= o) inc += t;
+                }
+                const uint64_t exc = inc - tv;
                 uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
 #pragma unroll 1
                 for (uint32_t at = 0; at < kf; ++at) {
@@ -599,20 +625,10 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
                     const uint32_t g1 = idx >= nU, g2 = idx >= nU + nV;
                     const int X = (int)(g1 + g2);
                     const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
-                    // the word holding row i: scan of the word totals
-                    uint32_t tv = 0;
-                    if (lane < nwd) {
-                        const uint32_t t0 = s.tw[lane], t1 = s.tw[nwd + lane];
-                        tv = X == 0 ? (t0 & 0xFFFFu) : (X == 1 ? (t0 >> 16) : t1);
-                    }
-                    uint32_t inc = tv;
-#pragma unroll
-                    for (int o = 1; o < 16; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(FULL, inc, o);
-                        if (lane >= o) inc += t;
-                    }
-                    const int wsel = __ffs(__ballot_sync(FULL, lane < nwd && inc > qq)) - 1;
-                    const uint32_t q1 = qq - __shfl_sync(FULL, inc - tv, wsel);
+                    // the word holding row i
+                    const int sh = 21 * X;
+                    const int wsel = __ffs(__ballot_sync(FULL, lane < nwd && ((uint32_t)(inc >> sh) & 0x1FFFFFu) > qq)) - 1;
+                    const uint32_t q1 = qq - ((uint32_t)(__shfl_sync(FULL, exc, wsel) >> sh) & 0x1FFFFFu);
                     // row i inside the word: scan of its later counts
                     const int lw = 32 * wsel + lane;
                     const uint32_t lv = lw < r ? (uint32_t)getf(s.lc[lw], X) : 0u;
@@ -625,17 +641,25 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
                     const int L = __ffs(__ballot_sync(FULL, inc2 > q1)) - 1;
                     const int i = 32 * wsel + L;
                     // j: the (q1 - acc)-th later member of row i's X class
+                    const uint16_t *nxX = s.nxh + X * RM;
                     int j = i;
-                    for (uint32_t hops = q1 - __shfl_sync(FULL, inc2 - lv, L) + 1; hops; --hops) j = getf(s.nx[j], X);
+#pragma unroll 1
+                    for (uint32_t hops = q1 - __shfl_sync(FULL, inc2 - lv, L) + 1; hops; --hops) j = nxX[j];
                     const int al = d ? j : i, be = d ? i : j;
                     // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e
                     const unsigned yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
                     const int Y = yz & 3, Z = yz >> 2;
-                    const bool sneg = P::RING == FG_ZT && X == 2 && (s.wsg(al) != s.wsg(be));
+                    const uint32_t sga = s.wsg(al), sgb = s.wsg(be);
+                    const bool sneg = P::RING == FG_ZT && X == 2 && sga != sgb;
                     bool v = true;
-                    const F yb = s.full(Y, be);
-                    const F ny = P::add(s.full(Y, al), P::sel(sneg, P::neg(yb), yb), v);   // y_a + s y_b
-                    const F nz = P::sub(s.full(Z, be), s.full(Z, al), v);                  // z_b - z_a
+                    const F ya = s.key(Y, al), yb = s.key(Y, be), za = s.key(Z, al), zb = s.key(Z, be);
+                    // the actual w carries its sign bit (stored up to sign)
+                    const F yaF = P::sel(Y == 2 && sga, P::neg(ya), ya);
+                    const F ybF = P::sel(Y == 2 && sgb, P::neg(yb), yb);
+                    const F zaF = P::sel(Z == 2 && sga, P::neg(za), za);
+                    const F zbF = P::sel(Z == 2 && sgb, P::neg(zb), zb);
+                    const F ny = P::add(yaF, P::sel(sneg, P::neg(ybF), ybF), v);   // y_a + s y_b
+                    const F nz = P::sub(zbF, zaF, v);                              // z_b - z_a
                     if (!v) continue;
                     alpha = al;
                     beta = be;
@@ -653,18 +677,18 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
             if (ok) {
                 // ---- commit (A4/A5): row alpha's Y := ny, row beta's Z := nz, R6 per row:
                 // only the changed factor can be first-negative; w absorbs the sign ----
+                const int fX = 3 - fY - fZ;
                 const bool fa = P::first_neg(fny), fb = P::first_neg(fnz);
                 const F kY = fY == 2 ? P::abs(fny) : P::sel(fa, P::neg(fny), fny);
                 const F kZ = fZ == 2 ? P::abs(fnz) : P::sel(fb, P::neg(fnz), fnz);
                 const uint32_t sa = fY == 2 ? (uint32_t)fa : (s.wsg(alpha) ^ (uint32_t)fa);
                 const uint32_t sb = fZ == 2 ? (uint32_t)fb : (s.wsg(beta) ^ (uint32_t)fb);
                 const F oY = s.key(fY, alpha), oZ = s.key(fZ, beta);
-                // the touched rows' keys after the commit (R12 test)
-                F A0 = s.key(0, alpha), A1 = s.key(1, alpha), A2 = s.key(2, alpha);
-                F B0 = s.key(0, beta), B1 = s.key(1, beta), B2 = s.key(2, beta);
-                A0 = P::sel(fY == 0, kY, A0); A1 = P::sel(fY == 1, kY, A1); A2 = P::sel(fY == 2, kY, A2);
-                B0 = P::sel(fZ == 0, kZ, B0); B1 = P::sel(fZ == 1, kZ, B1); B2 = P::sel(fZ == 2, kZ, B2);
+                // R12 test keys: alpha after the commit = (AX, kY, AZ), beta = (AX, BY, kZ)
+                // (alpha and beta share the X key: they are in one X class)
+                const F AX = s.key(fX, alpha), AZ = s.key(fZ, alpha), BY = s.key(fY, beta);
                 const bool zY = P::zero(kY), zZ = P::zero(kZ);
+                const F *pX = s.fac + fX * RM, *pY = s.fac + fY * RM, *pZ = s.fac + fZ * RM;
                 // fused compare pass: class updates of (alpha, Y) and (beta, Z) + R12 test
                 int pO0 = NIL, sO0 = NIL, pK0 = NIL, sK0 = NIL, aK0 = 0, tD0 = 0;
                 int pO1 = NIL, sO1 = NIL, pK1 = NIL, sK1 = NIL, aK1 = 0, tD1 = 0;
@@ -672,22 +696,20 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
 #pragma unroll 1
                 for (int w = 0; w < nwd; ++w) {
                     const int l = 32 * w + lane;
-                    const bool live = l < r;
-                    const F f0 = s.fac[l], f1 = s.fac[RM + l], f2 = s.fac[2 * RM + l];
-                    const F xY = fY == 0 ? f0 : (fY == 1 ? f1 : f2);
-                    const F xZ = fZ == 0 ? f0 : (fZ == 1 ? f1 : f2);
-                    const bool la = live && l != alpha, lb = live && l != beta;
-                    const bool eo0 = la && P::eq(xY, oY), ek0 = la && !zY && P::eq(xY, kY);
-                    const bool eo1 = lb && P::eq(xZ, oZ), ek1 = lb && !zZ && P::eq(xZ, kZ);
-                    const int ca = (int)P::eq(f0, A0) + (int)P::eq(f1, A1) + (int)P::eq(f2, A2);
-                    const int cb = (int)P::eq(f0, B0) + (int)P::eq(f1, B1) + (int)P::eq(f2, B2);
-                    hit = hit || (la && lb && (ca >= 2 || cb >= 2));
-                    const uint32_t mO0 = __ballot_sync(FULL, eo0), mK0 = __ballot_sync(FULL, ek0);
-                    const uint32_t mO1 = __ballot_sync(FULL, eo1), mK1 = __ballot_sync(FULL, ek1);
+                    const F xX = pX[l], xY = pY[l], xZ = pZ[l];
+                    const bool la = l < r && l != alpha, lb = l < r && l != beta;
+                    const bool yO = P::eq(xY, oY), yK = P::eq(xY, kY), yB = P::eq(xY, BY);
+                    const bool zO = P::eq(xZ, oZ), zK = P::eq(xZ, kZ), zA = P::eq(xZ, AZ);
+                    const bool xA = P::eq(xX, AX);
+                    // two shared factors with alpha (yK, zA, xA) or with beta (yB, zK, xA)
+                    const bool two = (yK && (zA || xA)) || (zA && xA) || (yB && (zK || xA)) || (zK && xA);
+                    hit = hit || (la && lb && two);
+                    const uint32_t mO0 = __ballot_sync(FULL, la && yO), mK0 = __ballot_sync(FULL, la && yK);
+                    const uint32_t mO1 = __ballot_sync(FULL, lb && zO), mK1 = __ballot_sync(FULL, lb && zK);
                     if ((mO0 | mK0 | mO1 | mK1) == 0u) continue;
                     uint32_t dl = 0;
-                    if (l < alpha && eo0 != ek0) dl += ek0 ? (1u << (10 * fY)) : (0u - (1u << (10 * fY)));
-                    if (l < beta && eo1 != ek1) dl += ek1 ? (1u << (10 * fZ)) : (0u - (1u << (10 * fZ)));
+                    if (l < alpha && la && yO != yK) dl += yK ? (1u << (10 * fY)) : (0u - (1u << (10 * fY)));
+                    if (l < beta && lb && zO != zK) dl += zK ? (1u << (10 * fZ)) : (0u - (1u << (10 * fZ)));
                     if (dl) s.lc[l] += dl;
                     {
                         const uint32_t bl = below_in(alpha, w), ab = above_in(alpha, w);
@@ -716,27 +738,29 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
                 __syncwarp();
                 if (lane == 0) {
                     // (alpha, Y) and (beta, Z): different roles, disjoint fields
-                    if (pO0 != NIL) s.nx[pO0] = setf(s.nx[pO0], fY, sO0);
-                    if (pK0 != NIL) s.nx[pK0] = setf(s.nx[pK0], fY, alpha);
-                    s.nx[alpha] = (setf(s.nx[alpha], fY, sK0) & ~WSIGN) | (sa ? WSIGN : 0u);
+                    if (pO0 != NIL) s.set_nxt(fY, pO0, sO0);
+                    if (pK0 != NIL) s.set_nxt(fY, pK0, alpha);
+                    s.set_nxt(fY, alpha, sK0);
                     const int old0 = getf(s.lc[alpha], fY);
                     s.lc[alpha] = setf(s.lc[alpha], fY, aK0);
                     s.tw_add(alpha >> 5, fY, aK0 - old0);
                     s.fac[fY * RM + alpha] = kY;
-                    if (pO1 != NIL) s.nx[pO1] = setf(s.nx[pO1], fZ, sO1);
-                    if (pK1 != NIL) s.nx[pK1] = setf(s.nx[pK1], fZ, beta);
-                    s.nx[beta] = (setf(s.nx[beta], fZ, sK1) & ~WSIGN) | (sb ? WSIGN : 0u);
+                    if (pO1 != NIL) s.set_nxt(fZ, pO1, sO1);
+                    if (pK1 != NIL) s.set_nxt(fZ, pK1, beta);
+                    s.set_nxt(fZ, beta, sK1);
                     const int old1 = getf(s.lc[beta], fZ);
                     s.lc[beta] = setf(s.lc[beta], fZ, aK1);
                     s.tw_add(beta >> 5, fZ, aK1 - old1);
                     s.fac[fZ * RM + beta] = kZ;
+                    s.set_wsg(alpha, sa);
+                    s.set_wsg(beta, sb);
                 }
                 __syncwarp();
                 nCU += (fY == 0 ? (uint32_t)tD0 : 0u) + (fZ == 0 ? (uint32_t)tD1 : 0u);
                 nCV += (fY == 1 ? (uint32_t)tD0 : 0u) + (fZ == 1 ? (uint32_t)tD1 : 0u);
                 nCW += (fY == 2 ? (uint32_t)tD0 : 0u) + (fZ == 2 ? (uint32_t)tD1 : 0u);
-                const int same = (int)P::eq(A0, B0) + (int)P::eq(A1, B1) + (int)P::eq(A2, B2);
-                need_local = zY || zZ || hit || same >= 2;
+                // the pair itself: X shared, plus Y (kY vs BY) or Z (AZ vs kZ)
+                need_local = zY || zZ || hit || P::eq(kY, BY) || P::eq(AZ, kZ);
             }
 
             uint32_t exp_flag = 0;
@@ -810,14 +834,15 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
         // ---------------- store the walker and its class image ----------------
         store_rows(a.cur + (size_t)wk * FG_PLANES * R);
         if (img) {
+            uint32_t *nxi = img, *lci = img + 3 * RM / 2, *twi = lci + RM;
 #pragma unroll 1
-            for (int l = lane; l < RM; l += 32) {
-                img[l] = s.nx[l];
-                img[RM + l] = s.lc[l];
-            }
-            if (lane < 2 * nwd) img[2 * RM + lane] = s.tw[lane];
+            for (int k = lane; k < 3 * RM / 2; k += 32) nxi[k] = reinterpret_cast<const uint32_t *>(s.nxh)[k];
+#pragma unroll 1
+            for (int l = lane; l < RM; l += 32) lci[l] = s.lc[l];
+            twi[lane] = s.tw[lane];
+            if (lane < 16) twi[32 + lane] = s.wsb[lane];
             if (lane == 0) {
-                uint32_t *sc = img + 2 * RM + 2 * nwd;
+                uint32_t *sc = twi + 48;
                 sc[0] = nCU; sc[1] = nCV; sc[2] = nCW;
                 sc[3] = (uint32_t)dset; sc[4] = (uint32_t)(dset >> 32);
                 sc[5] = (uint32_t)nD; sc[6] = dover ? 1u : 0u;
@@ -855,10 +880,12 @@ __global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
     }
 }
 
-// shared memory per warp: factors, nx, lc, word totals (2 x 16), Philox table, counters
+// shared memory per warp: factors, lc, word totals (32), sign bits (16), Philox table,
+// counters, next arrays (3 x RM u16)
 template <class P> size_t wl_smem(int nwd)
 {
-    return (size_t)3 * 32 * nwd * sizeof(typename P::F) + 2 * 32 * nwd * 4 + 2 * 16 * 4 + 32 * PXS * 4 + 8 * 4;
+    return (size_t)3 * 32 * nwd * sizeof(typename P::F) + 32 * nwd * 4 + 32 * 4 + 16 * 4 + 32 * PXS * 4 + 8 * 4 +
+           3 * 32 * nwd * 2;
 }
 
 template <class P>
