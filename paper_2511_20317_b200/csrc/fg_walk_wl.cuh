@@ -25,6 +25,8 @@
 // Same readings (R8-R23), draw order and digest as the oracle and the other kernels;
 // parity: tests/test_gpu_parity.py, tests/test_gpu_fullsize.py, tests/test_gpu_fuzz.py.
 #pragma once
+#include <cstdlib>
+#include <type_traits>
 #include "fg_device.cuh"
 
 namespace fgwl {
@@ -232,8 +234,8 @@ __device__ __noinline__ uint32_t check_structure(WS<P> s, int r, uint32_t nCU, u
     return __reduce_or_sync(FULL, bad);
 }
 
-template <class P>
-__global__ void __launch_bounds__(32) walk_wl(WalkArgs a, int nwd)
+template <class P, int MINB>
+__global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
 {
     typedef typename P::F F;
     extern __shared__ __align__(16) unsigned char smraw[];
@@ -888,22 +890,39 @@ template <class P> size_t wl_smem(int nwd)
            3 * 32 * nwd * 2;
 }
 
-template <class P>
-cudaError_t launch_wl(const WalkArgs &a, int num_sms, cudaStream_t st)
+template <class P, int MINB>
+cudaError_t launch_wl_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     const int nwd = (a.R + 31) / 32;
     if (nwd > 16) return cudaErrorInvalidValue;
     const size_t smem = wl_smem<P>(nwd);
-    cudaError_t e = cudaFuncSetAttribute(walk_wl<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(walk_wl<P, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int bps = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_wl<P>, 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_wl<P, MINB>, 32, smem);
     if (e != cudaSuccess) return e;
     if (bps < 1) bps = 1;
     int64_t blocks = (int64_t)num_sms * bps;
     if (blocks > a.num_walkers) blocks = a.num_walkers;
-    walk_wl<P><<<(unsigned)blocks, 32, smem, st>>>(a, nwd);
+    walk_wl<P, MINB><<<(unsigned)blocks, 32, smem, st>>>(a, nwd);
     return cudaGetLastError();
+}
+
+// register budget (resident warps per SM the compiler must allow): FG_WL_MINB selects
+// an instantiation for A/B timing
+template <class P>
+cudaError_t launch_wl(const WalkArgs &a, int num_sms, cudaStream_t st)
+{
+    const char *ev = getenv("FG_WL_MINB");
+    const int mb = ev ? atoi(ev) : 0;
+    if (mb == 1) return launch_wl_m<P, 1>(a, num_sms, st);
+    if (mb == 20) return launch_wl_m<P, 20>(a, num_sms, st);
+    if (mb == 24) return launch_wl_m<P, 24>(a, num_sms, st);
+    if (mb == 16) return launch_wl_m<P, 16>(a, num_sms, st);
+    // measured (scripts/gpu_r02_minb.sh): P32 (C4) runs best with 20 resident warps' worth
+    // of registers (96), the P64 layouts with 16 (128 registers; 96 spills too much)
+    if (std::is_same<P, P32>::value) return launch_wl_m<P, 20>(a, num_sms, st);
+    return launch_wl_m<P, 16>(a, num_sms, st);
 }
 
 }  // namespace fgwl
