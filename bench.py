@@ -40,6 +40,10 @@ def parse():
                     help="--impl reference: total oracle time budget over warmup + steps")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", help="nccl (default); gloo only for tests")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the other BASELINE workloads")
+    ap.add_argument("--per-config-steps", type=int, default=4, help="timed phases per other workload")
+    ap.add_argument("--per-config-ladder-s", type=float, default=3.0,
+                    help="device seconds each other workload walks for its time-to-rank ladder")
     return ap.parse_args()
 
 
@@ -49,6 +53,13 @@ def parse():
 NCU_TRAFFIC = {
     ("walk_q4<P16>", "c2_333_zt"): (52.551424e6 + 7.051776e6, "profiles/r01_ncu_walk_q4.txt", 58.89, 50.5),
 }
+
+
+# phase length of the multi-row configs (C3-C5)
+PHASE_MULTI = 2000
+# LOP3/IADD chain rate measured on the B200 relative to the ALU-pipe model (2.517 vs 2.0
+# warp-instructions per clock per SM, profiles/r01_microbench.txt)
+MEASURED_INT_RATIO = 2.517 / 2.0
 
 
 def model_ops_per_step(ring: int, r: float) -> float:
@@ -154,6 +165,152 @@ def reference_arm(args, wl):
     print(json.dumps(out), flush=True)
 
 
+# ---------------- time to rank (exact) ----------------
+def ladder_from_first(first, phase_ms, S, naive_rank, seeded_rank=None):
+    """Time-to-rank from the first step index of a verified strict improvement to each
+    rank (fg_rank_first_steps, min over ranks): rank <= t is first held after step
+    s* = min_{k <= t} first[k]; its device time is the phases before s*'s phase plus
+    the fraction (s* + 1) / S of that phase (uniform progress within a phase).
+    Returns {t: (seconds, steps done per walker)} for every reached t < naive_rank."""
+    out = {}
+    best = None
+    top = min(len(first), naive_rank)
+    cum = [0.0]
+    for ms in phase_ms:
+        cum.append(cum[-1] + ms / 1000.0)
+    for t in range(top):
+        if first[t] < (1 << 63) and (best is None or first[t] < best):
+            best = int(first[t])
+        if best is None:
+            continue
+        p = best // S
+        if p >= len(phase_ms):
+            continue
+        if seeded_rank is not None and t >= seeded_rank:
+            continue
+        out[t] = (cum[p] + (best - p * S + 1) / S * phase_ms[p] / 1000.0, best + 1)
+    return out
+
+
+def roofline_of(g, wl, W, S, walk_ms, launches, total_ms, r_mean, clk):
+    per_launch_ms = walk_ms / max(1, launches)
+    ops = model_ops_per_step(wl.ring, r_mean) * W * S       # per launch
+    achieved = ops / (per_launch_ms / 1000.0) / 1e12
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    peak = int_peak_tops(sm_mhz)
+    # DRAM bytes per launch from the committed `ncu --set full` capture of this kernel
+    # on this workload (dram__bytes_read.sum + dram__bytes_write.sum), if there is one
+    traffic = NCU_TRAFFIC.get((g.kernel_name, wl.key))
+    return {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
+            "frac": achieved / peak, "traffic": traffic[0] if traffic else None,
+            "traffic_unit": "B/launch", "traffic_source": traffic[1] if traffic else None,
+            "ncu_issue_active_pct": traffic[2] if traffic else None,
+            "ncu_alu_pipe_pct": traffic[3] if traffic else None,
+            "kernel": g.kernel_name, "kernel_ms_per_launch": per_launch_ms,
+            "kernel_share_of_step": walk_ms / total_ms if total_ms else None,
+            "ops_per_step_model": model_ops_per_step(wl.ring, r_mean),
+            "frac_vs_measured_int_rate": achieved / (peak * MEASURED_INT_RATIO),
+            "peak_basis": f"ALU pipe only: 148 SMs x 64 int32 lanes/clk x {sm_mhz:.0f} MHz (median under "
+                          f"load); the LOP3/IADD chain measures {MEASURED_INT_RATIO:.3f}x that "
+                          "(profiles/r01_microbench.txt: ptxas moves IADDs to the FMA pipe)"}
+
+
+class Run:
+    """One workload on this rank: seed, warm up, time phases (CUDA events on the libfg
+    stream), keep the per-phase times for the time-to-rank ladder."""
+
+    def __init__(self, wl, W, S, rank, world, dev, stream, fg, PoolSync):
+        self.wl, self.W, self.S, self.world = wl, W, S, world
+        self.stream = stream
+        self.g = fg.FlipGraph(wl.m, wl.n, wl.p, wl.ring, wl.r_cap, W, rank * W, dev, stream.cuda_stream)
+        self.sync = PoolSync(self.g, world)
+        self.g.seed_naive()
+        self.phase_ms = []
+
+    def phase(self):
+        import torch
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(self.stream)
+        self.g.walk(self.S, self.wl.seed)
+        best = self.sync.exchange()
+        ev1.record(self.stream)
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1)
+        self.phase_ms.append(ms)
+        return ms, best
+
+    def ladder(self, dist=None, dev="cpu"):
+        """Exact time-to-rank, box-wide (min over ranks of the first steps; times are
+        the max-over-ranks phase times)."""
+        import numpy as np
+        import torch
+        first = self.g.rank_first_steps(self.wl.r_cap).astype(np.float64)
+        ms = list(self.phase_ms)
+        if self.world > 1 and dist is not None:
+            t = torch.tensor(np.minimum(first, 2.0 ** 62), dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            first = t.cpu().numpy()
+            tm = torch.tensor(ms, dtype=torch.float64, device=dev)
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            ms = tm.cpu().tolist()
+        first_i = [int(x) if x < 2.0 ** 62 else (1 << 64) - 1 for x in first]
+        naive = self.wl.m * self.wl.n * self.wl.p
+        return ladder_from_first(first_i, ms, self.S, naive, seeded_rank=naive)
+
+
+def per_config(args, fg, PoolSync, dev, stream, clk_peak_mhz, skip):
+    """Every other BASELINE workload on this GPU (rank 0, N = 1): throughput, roofline
+    fraction of its kernel, exact time-to-rank ladder over a fixed device-time budget
+    and the best (rank, additions) reached."""
+    import torch
+    from paper_2511_20317_b200.inputs import WORKLOADS
+    out = {}
+    for key, wl in WORKLOADS.items():
+        if key == skip:
+            continue
+        S = 10000 if wl.r_cap <= 32 else PHASE_MULTI
+        run = Run(wl, wl.walkers, S, 0, 1, dev, stream, fg, PoolSync)
+        g = run.g
+        for _ in range(2):
+            run.phase()
+        st0 = g.stats()
+        r0 = g.get_walkers(rows=False)["r"].mean()
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        times = []
+        for _ in range(args.per_config_steps):
+            flush.zero_()
+            times.append(run.phase()[0])
+        st1 = g.stats()
+        r1 = g.get_walkers(rows=False)["r"].mean()
+        # keep walking (untimed for the value) to extend the time-to-rank ladder
+        budget = args.per_config_ladder_s * 1000.0
+        while sum(run.phase_ms) < budget:
+            run.phase()
+        total = sum(times)
+        value = float(wl.walkers) * S * len(times) / (total / 1000.0)
+        walk_ms = (st1["walk_us"] - st0["walk_us"]) / 1000.0
+        launches = st1["walk_launches"] - st0["walk_launches"]
+        roof = roofline_of(g, wl, wl.walkers, S, walk_ms, launches, total, 0.5 * (r0 + r1),
+                           {"sm_mhz": clk_peak_mhz})
+        best = g.best()
+        lad = run.ladder()
+        out[key] = {"workload": wl.name, "walkers": wl.walkers, "phase_steps": S,
+                    "value": value, "unit": "flip-steps/s", "ms_per_phase": total / len(times),
+                    "kernel": g.kernel_name, "kernel_ms_per_launch": roof["kernel_ms_per_launch"],
+                    "frac": roof["frac"], "traffic": roof["traffic"],
+                    "ncu_issue_active_pct": roof["ncu_issue_active_pct"],
+                    "best": {"rank": best["rank"], "additions": best["additions"]},
+                    "ladder_device_s": round(sum(run.phase_ms) / 1000.0, 3),
+                    "time_to_rank_s": {str(k): round(v[0], 6) for k, v in sorted(lad.items())},
+                    "target_rank": wl.target_rank,
+                    "verify_fail": st1["verify_fail"]}
+        g.close()
+        del flush
+        torch.cuda.synchronize()
+    return out
+
+
 # ---------------- our arm ----------------
 def main():
     args = parse()
@@ -163,7 +320,6 @@ def main():
         reference_arm(args, wl)
         return
 
-    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -180,39 +336,17 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
         else:
             dist.init_process_group(args.dist_backend)
+    rdev = "cuda" if args.dist_backend == "nccl" else "cpu"
     stream = torch.cuda.current_stream()
     W = args.walkers or wl.walkers
-    g = fg.FlipGraph(wl.m, wl.n, wl.p, wl.ring, wl.r_cap, W, rank * W, dev, stream.cuda_stream)
-    sync = PoolSync(g, world)
-    g.seed_naive()
     S = args.phase_steps
+    run = Run(wl, W, S, rank, world, dev, stream, fg, PoolSync)
+    g = run.g
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
-
-    # time-to-rank ladder: device time since seeding until the box best first <= rank
-    ladder = {}
-    ladder_steps = {}            # box walker-steps done when each rank was first reached
-    elapsed = [0.0]
-    done_steps = [0]
-
-    def phase(timed_events=None):
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
-        ev0.record(stream)
-        g.walk(S, wl.seed)
-        best = sync.exchange()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        ms = ev0.elapsed_time(ev1)
-        elapsed[0] += ms / 1000.0
-        done_steps[0] += W * S * world
-        for target in range(best["rank"], wl.m * wl.n * wl.p):
-            ladder.setdefault(target, elapsed[0])
-            ladder_steps.setdefault(target, done_steps[0])
-        return ms
 
     for _ in range(args.warmup):
         flush.zero_()
-        phase()
+        run.phase()
     st0 = g.stats()
     r_before = g.get_walkers(rows=False)["r"].mean()
     clocks = Clocks(dev)
@@ -222,7 +356,7 @@ def main():
     times = []
     for _ in range(args.steps):
         flush.zero_()                       # L2 flushed between timed steps (not timed)
-        times.append(phase())
+        times.append(run.phase()[0])
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -230,8 +364,7 @@ def main():
     st1 = g.stats()
     r_after = g.get_walkers(rows=False)["r"].mean()
     total_ms = sum(times)
-    t = torch.tensor([total_ms], dtype=torch.float64,
-                     device="cuda" if args.dist_backend == "nccl" else "cpu")
+    t = torch.tensor([total_ms], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
@@ -241,24 +374,8 @@ def main():
     # dominant kernel (walk) timed live with CUDA events inside libfg, on its stream
     walk_ms = (st1["walk_us"] - st0["walk_us"]) / 1000.0
     launches = st1["walk_launches"] - st0["walk_launches"]
-    per_launch_ms = walk_ms / max(1, launches)
-    r_mean = 0.5 * (r_before + r_after)
-    ops = model_ops_per_step(wl.ring, r_mean) * W * S       # per launch
-    achieved = ops / (per_launch_ms / 1000.0) / 1e12
-    sm_mhz = clk.get("sm_mhz") or 1965.0
-    peak = int_peak_tops(sm_mhz)
-    # DRAM bytes per launch from the committed `ncu --set full` capture of this kernel
-    # on this workload (dram__bytes_read.sum + dram__bytes_write.sum), if there is one
-    traffic = NCU_TRAFFIC.get((g.kernel_name, args.workload))
-    roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Tops/s",
-                "frac": achieved / peak, "traffic": traffic[0] if traffic else None,
-                "traffic_unit": "B/launch", "traffic_source": traffic[1] if traffic else None,
-                "ncu_issue_active_pct": traffic[2] if traffic else None,
-                "ncu_alu_pipe_pct": traffic[3] if traffic else None,
-                "kernel": g.kernel_name, "kernel_ms_per_launch": per_launch_ms,
-                "kernel_share_of_step": walk_ms / total_ms if total_ms else None,
-                "ops_per_step_model": model_ops_per_step(wl.ring, r_mean),
-                "peak_basis": f"148 SMs x 64 int32 lanes/clk x {sm_mhz:.0f} MHz (median under load)"}
+    roofline = roofline_of(g, wl, W, S, walk_ms, launches, total_ms, 0.5 * (r_before + r_after), clk)
+    lad = run.ladder(dist if world > 1 else None, rdev)
 
     # e2e through the C ABI with host buffers: H2D state, walk, D2H state every step
     e2e = None
@@ -273,12 +390,11 @@ def main():
             t0 = time.perf_counter()
             g.load_state(host.data_ptr())
             g.walk(S, wl.seed)
-            sync.exchange()
+            run.sync.exchange()
             g.save_state(host.data_ptr())
             torch.cuda.synchronize()
             e_times.append(time.perf_counter() - t0)
-        te = torch.tensor([sum(e_times)], dtype=torch.float64,
-                          device="cuda" if args.dist_backend == "nccl" else "cpu")
+        te = torch.tensor([sum(e_times)], dtype=torch.float64, device=rdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": float(W) * S * len(e_times) * world / float(te.item()), "unit": "flip-steps/s",
@@ -289,11 +405,15 @@ def main():
         cpu = run_oracle_sample(wl, args.cpu_seconds)
         # the trajectories are identical on the CPU (parity), so the oracle reaches each
         # rank after the same walker-steps: time = steps / its measured rate (extrapolated)
-        cpu["time_to_rank_s_extrapolated"] = {str(k): round(v / cpu["value"], 1)
-                                              for k, v in sorted(ladder_steps.items())}
+        cpu["time_to_rank_s_extrapolated"] = {str(k): round(v[1] * W * world / cpu["value"], 2)
+                                              for k, v in sorted(lad.items())}
 
     best = g.best()
     stats = {k: st1[k] - st0[k] for k in ("verified", "verify_fail", "queue_overflow")}
+    g.close()
+    pc = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        pc = per_config(args, fg, PoolSync, dev, stream, clk.get("sm_mhz") or 1965.0, args.workload)
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "flip-steps/s", "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -301,15 +421,16 @@ def main():
                "data": "synthetic",
                "config": {"workload": wl.name, "walkers_per_gpu": W, "phase_steps": S,
                           "seed": hex(wl.seed), "l2": "flushed (256 MB write) between timed steps",
-                          "kernel": g.kernel_name},
+                          "kernel": roofline["kernel"]},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(st1["launches"] - st0["launches"]),
                "clocks": clk,
-               "time_to_rank_s": {str(k): round(v, 4) for k, v in sorted(ladder.items())},
+               "time_to_rank_s": {str(k): round(v[0], 6) for k, v in sorted(lad.items())},
+               "time_to_rank_basis": "exact: first step index of a verified strict improvement "
+                                     "(fg_rank_first_steps), device time interpolated within its phase",
                "best": {"rank": best["rank"], "additions": best["additions"]},
-               "verify": stats}
+               "verify": stats, "per_config": pc}
         print(json.dumps(out), flush=True)
-    g.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -35,6 +35,11 @@ class Workload:
     def fmt(self):
         return (self.m, self.n, self.p)
 
+    @property
+    def key(self) -> str:
+        """The WORKLOADS key of this workload ("c2_333_zt", ...)."""
+        return next(k for k, v in WORKLOADS.items() if v is self)
+
 
 # BASELINE.json configs; R from SURVEY.md section 8(a); targets PAPER:11, PAPER:65, PAPER:699
 WORKLOADS = {

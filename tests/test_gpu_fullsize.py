@@ -227,3 +227,30 @@ def test_local_best_keeps_fewer_additions(fg, orc):
         seen.append((b["rank"], b["additions"], b["walker_id"]))
     for x, y in zip(seen, seen[1:]):
         assert y <= x, seen
+
+
+def test_rank_first_steps_match_oracle(fg, orc):
+    """Exact time-to-rank (fg_rank_first_steps): on C1, the first step index at which
+    any walker's best reaches each rank equals the oracle's, found by stepping every
+    oracle walker one iteration at a time."""
+    wl = WORKLOADS["c1_222_zt"]
+    W, steps = 64, 30000
+    g = _ctx(fg, 2, 2, 2, ZT, wl.r_cap, W)
+    g.seed_naive()
+    g.walk(steps, wl.seed, fg.params_default(phase_steps=7000))
+    first = g.rank_first_steps(8)
+    U = (1 << 64) - 1
+    exp = [U] * 9
+    exp[8] = 0
+    for k in range(W):
+        w = orc.walker(2, 2, 2, ZT, wl.r_cap, walker_id=k)
+        w.seed_naive()
+        b = 8
+        for s in range(steps):
+            w.walk(1, wl.seed)
+            if w.best_r < b:
+                b = w.best_r
+                exp[b] = min(exp[b], s)
+            if b == 7:
+                break
+    assert [int(x) for x in first] == exp, (first, exp)
