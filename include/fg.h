@@ -253,6 +253,13 @@ int fg_lift(int m, int n, int p, const int8_t *z2, int rank, int64_t node_budget
    counts must hold 65^3 ints.  Host only. */
 int fg_type_invariant(int m, int n, int p, int ring, const int8_t *coeffs, int rank, int32_t *counts,
                       int32_t rank_sums[3]);
+/* Symmetrised polynomial invariant: sym[(a*65 + b)*65 + c] = the
+   coefficient of x^a y^b z^c in sum_{pi in S_3} pi(sum_i x^{rank U_i} y^{rank V_i}
+   z^{rank W_i}), ranks as in fg_type_invariant.  Invariant under the cyclic symmetry and
+   transposition (meta operators), unlike the type polynomial.  sym must hold 65^3
+   ints (caller-owned, overwritten).  FG_E_ARG on a NULL buffer, the fg_type_invariant
+   errors otherwise.  Host only. */
+int fg_sym_invariant(int m, int n, int p, int ring, const int8_t *coeffs, int rank, int32_t *sym);
 /* Canonical 64-bit key of a scheme up to row order and per-row sign normalisation
    (PAPER:429): for pool de-duplication.  Host only. */
 int fg_scheme_key(int m, int n, int p, int ring, const int8_t *coeffs, int rank, uint64_t *key);

@@ -93,6 +93,7 @@ void or_normalize_rows(int m, int n, int p, int8_t *coeffs, int rank);   /* PAPE
 int  or_naive(int m, int n, int p, int8_t *coeffs_out);   /* returns rank m*n*p */
 /* type invariant PAPER:516: out[(ru*65+rv)*65+rw] += 1 for each row; out has 65^3 ints */
 int  or_type_invariant(int m, int n, int p, const int8_t *coeffs, int rank, int32_t *out);
+int  or_sym_invariant(int m, int n, int p, const int8_t *coeffs, int rank, int32_t *out);
 int  or_matrix_rank(const int8_t *a, int rows, int cols);
 
 /* --- walker --- */

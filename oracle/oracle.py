@@ -74,6 +74,7 @@ class Oracle:
         lib.or_normalize_rows.argtypes = [i32, i32, i32, vp, i32]
         lib.or_naive.argtypes = [i32, i32, i32, vp]
         lib.or_type_invariant.argtypes = [i32, i32, i32, vp, i32, vp]
+        lib.or_sym_invariant.argtypes = [i32, i32, i32, vp, i32, vp]
         lib.or_matrix_rank.argtypes = [vp, i32, i32]
         lib.or_walker_init.argtypes = [vp, i32, i32, i32, i32, i32, u64]
         lib.or_walker_free.argtypes = [vp]
@@ -152,6 +153,19 @@ class Oracle:
             ru, rest = divmod(int(idx), 65 * 65)
             rv, rw = divmod(rest, 65)
             res[(ru, rv, rw)] = int(out[idx])
+        return res
+
+    def sym_invariant(self, m, n, p, coeffs):
+        """Symmetrised polynomial: {(a, b, c): coefficient of x^a y^b z^c}."""
+        c = np.ascontiguousarray(coeffs, dtype=np.int8)
+        out = np.zeros(65 ** 3, np.int32)
+        if self.lib.or_sym_invariant(m, n, p, _p(c), c.shape[0], _p(out)) != 0:
+            raise ValueError("or_sym_invariant failed")
+        res = {}
+        for idx in np.nonzero(out)[0]:
+            a, rest = divmod(int(idx), 65 * 65)
+            b, cc = divmod(rest, 65)
+            res[(a, b, cc)] = int(out[idx])
         return res
 
     # ---- meta operators: return ((m, n, p), coeffs) ----

@@ -153,3 +153,30 @@ int or_type_invariant(int m, int n, int p, const int8_t *coeffs, int rank, int32
     (void)pm;
     return 0;
 }
+
+/* Symmetrised polynomial: f(x,y,z) = sum_{pi in S_3} pi( sum_{i=1}^r
+ * x^{rank U_i} y^{rank V_i} z^{rank W_i} ).  Written term by term: each term i and each
+ * of the six permutations pi of (x, y, z) adds one monomial.  out[(a*65+b)*65+c] +=. */
+int or_sym_invariant(int m, int n, int p, const int8_t *coeffs, int rank, int32_t *out)
+{
+    static const int perms[6][3] = {{0,1,2},{0,2,1},{1,0,2},{1,2,0},{2,0,1},{2,1,0}};
+    int mn = m * n, np = n * p, width = mn + np + p * m, l, q;
+    for (l = 0; l < rank; l++) {
+        const int8_t *row = coeffs + (size_t)l * width;
+        int e[3];
+        e[0] = or_matrix_rank(row, m, n);             /* exponent of x: rank U_i */
+        e[1] = or_matrix_rank(row + mn, n, p);        /* exponent of y: rank V_i */
+        e[2] = or_matrix_rank(row + mn + np, p, m);   /* exponent of z: rank W_i */
+        if (e[0] < 0 || e[1] < 0 || e[2] < 0) return -1;
+        for (q = 0; q < 6; q++) {
+            /* pi maps the variables (x, y, z) -> (pi x, pi y, pi z): the exponent of
+               variable k after pi is the exponent of the variable pi sent to k */
+            int f[3];
+            f[perms[q][0]] = e[0];
+            f[perms[q][1]] = e[1];
+            f[perms[q][2]] = e[2];
+            out[(f[0] * 65 + f[1]) * 65 + f[2]] += 1;
+        }
+    }
+    return 0;
+}

@@ -83,15 +83,13 @@ struct VerifyArgs {
 // launchers (fg_walk.cu / fg_verify.cu); return cudaError_t
 enum fg_kernel_kind { FG_K_NONE = 0, FG_K_W32_ZT_K16, FG_K_W32_ZT_K32, FG_K_W32_Z2_K32,
                       FG_K_WM_P16, FG_K_WM_P32, FG_K_WM_P64, FG_K_WM_Z2, FG_K_WM_Z64,
-                      FG_K_H16_P16, FG_K_H16_P32, FG_K_H16_Z2, FG_K_T1_P16, FG_K_T1_Z2, FG_K_Q4_P16, FG_K_Q4_Z2, FG_K_QL_P16, FG_K_QL_Z2,
+                      FG_K_Q4_P16, FG_K_Q4_Z2, FG_K_QL_P16, FG_K_QL_Z2,
                       FG_K_WL_P16, FG_K_WL_P32, FG_K_WL_P64, FG_K_WL_Z2, FG_K_WL_Z64 };
 cudaError_t fg_launch_walk_wl(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 size_t fg_wl_img_words(int R);     // walk_wl class image words per walker
 bool fg_kind_is_wl(int kind);
 cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, cudaStream_t st);
-cudaError_t fg_launch_walk_t1(int kind, const WalkArgs &a, cudaStream_t st);
-cudaError_t fg_launch_walk_h16(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 int fg_multi_ns(int R);
 int fg_multi_kind(int ring, int maxlen, int R);
 cudaError_t fg_launch_walk_multi(int kind, int ns, const WalkArgs &a, int num_sms, cudaStream_t st);

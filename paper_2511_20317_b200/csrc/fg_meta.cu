@@ -455,6 +455,28 @@ int fg_type_invariant(int m, int n, int p, int ring, const int8_t *coeffs, int r
     return FG_OK;
 }
 
+// symmetrised polynomial: f = sum over pi in S_3 of pi applied to the
+// type polynomial, i.e. every term (ru, rv, rw) contributes one monomial per permutation
+int fg_sym_invariant(int m, int n, int p, int ring, const int8_t *coeffs, int rank, int32_t *sym)
+{
+    if (!sym) return FG_E_ARG;
+    std::vector<int32_t> counts((size_t)65 * 65 * 65);
+    int32_t sums[3];
+    int rc = fg_type_invariant(m, n, p, ring, coeffs, rank, counts.data(), sums);
+    if (rc != FG_OK) return rc;
+    memset(sym, 0, sizeof(int32_t) * 65 * 65 * 65);
+    static const int perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int a = 0; a <= 8; ++a)            // factor ranks are <= min(dims) <= 8 (R1: mn <= 64)
+        for (int b = 0; b <= 8; ++b)
+            for (int c = 0; c <= 8; ++c) {
+                const int32_t k = counts[(a * 65 + b) * 65 + c];
+                if (!k) continue;
+                const int e[3] = {a, b, c};
+                for (const auto &q : perm) sym[(e[q[0]] * 65 + e[q[1]]) * 65 + e[q[2]]] += k;
+            }
+    return FG_OK;
+}
+
 // canonical key: rows sign-normalised (Z_T), sorted, hashed (FNV-1a over the words);
 // equal schemes up to row order and the sign rescaling of PAPER:429 share a key
 int fg_scheme_key(int m, int n, int p, int ring, const int8_t *coeffs, int rank, uint64_t *key)

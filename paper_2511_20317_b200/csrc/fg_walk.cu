@@ -577,24 +577,21 @@ cudaError_t launch_w32(const WalkArgs &a, int num_sms, cudaStream_t st)
 // R <= 32: one-word factors (Z_T <= 16 elements, Z_2 <= 32) run one walker per
 // quad (fg_walk_q4.cu); Z_T with 17..32 elements runs this file's one walker per
 // warp.  33 <= R <= 512: the multi-row kernel (fg_walk_multi.cu) with the narrowest
-// factor layout that fits.  FG_WALK_KERNEL=w32 / h16 / t1 force the one-walker-per-
-// warp / two-walkers-per-warp / one-walker-per-thread kernels for R <= 32 (all are
-// parity-exact; DESIGN.md section 4 compares them).
+// factor layout that fits.  FG_WALK_KERNEL=w32 forces the one-walker-per-warp kernel
+// for R <= 32 (parity-exact; DESIGN.md section 4 compares the mappings; the
+// one-walker-per-thread and two-walkers-per-warp variants measured there were
+// removed from the build in round 2 and live in the git history).
 int fg_pick_kernel(int ring, int maxlen, int R)
 {
     if (R <= 32) {
         if (maxlen > 32) return FG_K_NONE;
         const char *env = getenv("FG_WALK_KERNEL");
-        const bool h16 = env && strcmp(env, "h16") == 0;
         const bool w32 = env && strcmp(env, "w32") == 0;
-        const bool t1 = env && strcmp(env, "t1") == 0;
         if (ring == FG_ZT) {
-            if (h16) return maxlen <= 16 ? FG_K_H16_P16 : FG_K_H16_P32;
             if (maxlen > 16) return FG_K_W32_ZT_K32;
-            return w32 ? FG_K_W32_ZT_K16 : (t1 ? FG_K_T1_P16 : FG_K_Q4_P16);
+            return w32 ? FG_K_W32_ZT_K16 : FG_K_Q4_P16;
         }
-        if (h16) return FG_K_H16_Z2;
-        return w32 ? FG_K_W32_Z2_K32 : (t1 ? FG_K_T1_Z2 : FG_K_Q4_Z2);
+        return w32 ? FG_K_W32_Z2_K32 : FG_K_Q4_Z2;
     }
     // 33 <= R <= 128, one-word factors: the linked-class quad kernel (fg_walk_ql.cu),
     // faster than walk_wm on (4,4,4) Z_T and Z_2 (profiles/r01_bench_multi.txt);
@@ -618,11 +615,6 @@ int fg_pick_kernel(int ring, int maxlen, int R)
 int fg_kind_for_mode(int kind)
 {
     switch (kind) {
-    case FG_K_H16_P16:
-    case FG_K_T1_P16: return FG_K_W32_ZT_K16;
-    case FG_K_H16_P32: return FG_K_W32_ZT_K32;
-    case FG_K_H16_Z2:
-    case FG_K_T1_Z2: return FG_K_W32_Z2_K32;
     case FG_K_QL_P16: return FG_K_WM_P16;
     case FG_K_QL_Z2: return FG_K_WM_Z2;
     default: return kind;
@@ -640,11 +632,6 @@ const char *fg_kernel_kind_name(int kind)
     case FG_K_WM_P64: return "walk_wm<P64>";
     case FG_K_WM_Z2: return "walk_wm<PZ2>";
     case FG_K_WM_Z64: return "walk_wm<PZ64>";
-    case FG_K_H16_P16: return "walk_h16<P16>";
-    case FG_K_H16_P32: return "walk_h16<P32>";
-    case FG_K_H16_Z2: return "walk_h16<PZ2>";
-    case FG_K_T1_P16: return "walk_t1<P16>";
-    case FG_K_T1_Z2: return "walk_t1<PZ2>";
     case FG_K_Q4_P16: return "walk_q4<P16>";
     case FG_K_Q4_Z2: return "walk_q4<PZ2>";
     case FG_K_QL_P16: return "walk_ql<P16>";
@@ -664,11 +651,6 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_W32_ZT_K16: return launch_w32<P16>(a, num_sms, st);
     case FG_K_W32_ZT_K32: return launch_w32<P32>(a, num_sms, st);
     case FG_K_W32_Z2_K32: return launch_w32<PZ2>(a, num_sms, st);
-    case FG_K_H16_P16:
-    case FG_K_H16_P32:
-    case FG_K_H16_Z2: return fg_launch_walk_h16(kind, a, num_sms, st);
-    case FG_K_T1_P16:
-    case FG_K_T1_Z2: return fg_launch_walk_t1(kind, a, st);
     case FG_K_Q4_P16:
     case FG_K_Q4_Z2: return fg_launch_walk_q4(kind, a, st);
     case FG_K_QL_P16:

@@ -4,7 +4,7 @@
 //
 // Why: the one-walker-per-warp kernel (fg_walk.cu) replicates per-walker scalar
 // work on 32 lanes (~420 warp instructions per walker-step); one walker per thread
-// (fg_walk_t1.cu, 90) leaves a single warp per scheduler at the C2 population
+// (walk_t1, 90; removed in round 2, see git history) leaves a single warp per scheduler at the C2 population
 // (16384 walkers = 512 warps on 592 SMSPs, 22% issue, profiles/r01_ncu_walk_t1.txt)
 // and lets the slowest of 32 walkers set every loop's trip count (~6 flip draws per
 // step for 2 on average).  A quad is the middle: 4x the warps, and the quad splits

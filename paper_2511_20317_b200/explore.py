@@ -39,16 +39,31 @@ def scheme_additions(fmt, ring, coeffs) -> int:
 
 @dataclass
 class Registry:
-    """Best scheme per format: lexicographic (rank, additions)."""
+    """Best scheme per format: lexicographic (rank, additions).
+    `archive` is the persistent store of discoveries: every distinct scheme
+    ever offered, per format, de-duplicated by its canonical key (fg_scheme_key: equal up
+    to row order and the sign rescaling of PAPER:429), with its invariants
+     for novelty checks."""
+    ring: int = fg.FG_ZT
     best: dict = field(default_factory=dict)     # fmt -> (rank, additions, coeffs)
+    archive: dict = field(default_factory=dict)  # fmt -> {key: (rank, additions, coeffs)}
 
     def offer(self, fmt, rank, adds, coeffs):
+        c = np.array(coeffs, dtype=np.int8)
+        key = fg.fg_scheme_key(*fmt, self.ring, c)
+        self.archive.setdefault(fmt, {}).setdefault(key, (rank, adds, c))
         cur = self.best.get(fmt)
         if cur is None or (rank, adds) < (cur[0], cur[1]):
-            self.best[fmt] = (rank, adds, np.array(coeffs, dtype=np.int8))
+            self.best[fmt] = (rank, adds, c)
 
     def schemes(self):
         return [(f, v[2]) for f, v in sorted(self.best.items())]
+
+    def invariants(self, fmt, key):
+        """(type polynomial, rank sums, symmetrised polynomial) of an archived scheme."""
+        _, _, c = self.archive[fmt][key]
+        t, sums = fg.fg_type_invariant(*fmt, self.ring, c)
+        return t, sums, fg.fg_sym_invariant(*fmt, self.ring, c)
 
 
 class Explorer:
@@ -60,7 +75,7 @@ class Explorer:
         self.ring, self.seed, self.device, self.stream = ring, seed, device, stream
         self.thr_resize = thr_resize
         self.params = params
-        self.registry = Registry()
+        self.registry = Registry(ring)
         self.round_no = 0
         for f, c in self.pop:
             rc, _ = fg.fg_verify(*f, ring, c)
@@ -108,3 +123,7 @@ class Explorer:
 
     def formats(self):
         return sorted({f for f, _ in self.pop})
+
+    def diversity(self):
+        """Number of distinct schemes in the population (canonical keys)."""
+        return len({(f, fg.fg_scheme_key(*f, self.ring, c)) for f, c in self.pop})

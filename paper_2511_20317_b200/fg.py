@@ -83,6 +83,7 @@ _sig = {
                           _u64, _u64, _vp]),
     "fg_lift": (_i32, [_i32, _i32, _i32, _vp, _i32, _i64, _vp, _vp]),
     "fg_type_invariant": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp]),
+    "fg_sym_invariant": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
     "fg_scheme_key": (_i32, [_i32, _i32, _i32, _i32, _vp, _i32, _vp]),
 }
 for _name, (_res, _args) in _sig.items():
@@ -208,6 +209,19 @@ def fg_type_invariant(m, n, p, ring, coeffs):
         rv, rw = divmod(rest, 65)
         out[(ru, rv, rw)] = int(counts[idx])
     return out, tuple(int(x) for x in sums)
+
+
+def fg_sym_invariant(m, n, p, ring, coeffs):
+    """{(a, b, c): coefficient} of the symmetrised polynomial."""
+    c = np.ascontiguousarray(coeffs, dtype=np.int8)
+    sym = np.zeros(65 ** 3, np.int32)
+    _ck(_lib.fg_sym_invariant(m, n, p, ring, _p(c), c.shape[0], _p(sym)), "fg_sym_invariant")
+    out = {}
+    for idx in np.nonzero(sym)[0]:
+        a, rest = divmod(int(idx), 65 * 65)
+        b, cc = divmod(rest, 65)
+        out[(a, b, cc)] = int(sym[idx])
+    return out
 
 
 def fg_scheme_key(m, n, p, ring, coeffs) -> int:

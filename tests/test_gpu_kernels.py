@@ -1,6 +1,5 @@
 """Every R <= 32 walk kernel against the CPU oracle (FG_WALK_KERNEL selects it at
-fg_create): one walker per warp (w32), two per warp (h16), one per thread (t1) and
-one per quad (q4, the default).  Same bar as test_gpu_parity.py: bit-exact final and
+fg_create): one walker per warp (w32) and one per quad (q4, the default).  Same bar as test_gpu_parity.py: bit-exact final and
 best schemes, ranks, counters and the per-step event digest.
 
 Walker counts that are not multiples of 8 / 32 exercise the tail quads and warps.
@@ -15,7 +14,7 @@ from paper_2511_20317_b200.inputs import WORKLOADS, sample_walkers
 
 pytestmark = pytest.mark.gpu
 ZT, Z2 = 0, 1
-KERNELS = {"w32": "walk_w32", "h16": "walk_h16", "t1": "walk_t1", "q4": "walk_q4"}
+KERNELS = {"w32": "walk_w32", "q4": "walk_q4"}
 KERNEL_PREFIX = dict(KERNELS, ql="walk_ql", wm="walk_wm", wl="walk_wl")
 
 
@@ -86,7 +85,7 @@ def test_kernel_c2_sampled(fg, orc, kernel, ring):
     assert g.stats()["verify_fail"] == 0
 
 
-@pytest.mark.parametrize("kernel", ["t1", "q4"])
+@pytest.mark.parametrize("kernel", ["w32", "q4"])
 def test_kernel_small_rcap_and_edge(fg, orc, kernel):
     """R < 32 (expand hits the row cap) and a format with 1-element factors."""
     for (m, n, p, R, steps) in [((2), 2, 2, 9, 6000), (1, 2, 3, 8, 4000), (2, 3, 2, 14, 5000)]:
@@ -99,7 +98,7 @@ def test_kernel_small_rcap_and_edge(fg, orc, kernel):
         _check(got, ref, None)
 
 
-@pytest.mark.parametrize("kernel", ["w32", "t1", "q4"])
+@pytest.mark.parametrize("kernel", ["w32", "q4"])
 def test_kernel_k_flip_round_boundaries(fg, orc, kernel):
     """K (draws per try_flip, R11) below, at and across the quad kernel's 4-draw rounds,
     with a high expand rate so flip failures and expands are frequent."""

@@ -123,6 +123,15 @@ def test_invariants_match_oracle_and_paper(fg, orc):
     assert fg.fg_type_invariant(*nf, ZT, sq)[0] == orc.type_invariant(*nf, sq)
 
 
+def test_sym_invariant_matches_oracle(fg, orc):
+    """libfg's symmetrised polynomial equals the oracle's on every scheme."""
+    m, n, p, s = load_scheme("sec36_after.txt")
+    assert fg.fg_sym_invariant(m, n, p, ZT, s) == {(2, 2, 2): 6, (1, 1, 1): 36}
+    for fmt, ring, c in _schemes(orc):
+        if ring == ZT:
+            assert fg.fg_sym_invariant(*fmt, ring, c) == orc.sym_invariant(*fmt, c), fmt
+
+
 def test_scheme_key_is_invariant_under_row_order_and_sign(fg, orc):
     m, n, p, before = load_scheme("sec36_before.txt")
     _, _, _, after = load_scheme("sec36_after.txt")
@@ -154,3 +163,22 @@ def test_resize_alg2_matches_oracle(fg, orc):
         ops[op >> 1] += 1
     assert ops[1] > 0 and ops[2] + ops[3] + ops[4] + ops[5] > 50
     assert ops[3] > ops[4] > ops[2]             # product > double > project (50 / 30 / 5)
+
+
+def test_registry_archive_deduplicates(fg, orc):
+    """The archive (PAPER:291 persistent storage) holds each scheme once up to row order
+    and sign rescaling (fg_scheme_key); invariants come with it."""
+    from paper_2511_20317_b200.explore import Registry
+    m, n, p, before = load_scheme("sec36_before.txt")
+    _, _, _, after = load_scheme("sec36_after.txt")
+    reg = Registry(0)
+    reg.offer((2, 2, 2), 7, orc.additions(2, 2, 2, after), after)
+    reg.offer((2, 2, 2), 7, orc.additions(2, 2, 2, before), before)             # same scheme
+    reg.offer((2, 2, 2), 7, 18, after[np.random.default_rng(1).permutation(7)])  # row order
+    assert len(reg.archive[(2, 2, 2)]) == 1
+    reg.offer((2, 2, 2), 8, 4, orc.naive(2, 2, 2))
+    assert len(reg.archive[(2, 2, 2)]) == 2 and reg.best[(2, 2, 2)][0] == 7
+    key = next(iter(reg.archive[(2, 2, 2)]))
+    t, sums, sym = reg.invariants((2, 2, 2), key)
+    assert t == {(2, 2, 2): 1, (1, 1, 1): 6} and sums == (8, 8, 8)
+    assert sym == {(2, 2, 2): 6, (1, 1, 1): 36}

@@ -191,6 +191,45 @@ def test_t5_type_invariant_strassen(orc):
     assert orc.type_invariant(m, n, p, orc.naive(m, n, p)) == {(1, 1, 1): 27}
 
 
+# ---------------- symmetrised polynomial PAPER:519-521 ----------------
+def _add(acc, d):
+    for k, v in d.items():
+        acc[k] = acc.get(k, 0) + v
+    return acc
+
+
+def test_sym_invariant_strassen_and_group_orbit(orc):
+    """f on the rank-7 example = 6 x^2y^2z^2 + 36 xyz (the S_3 orbit of X^2Y^2Z^2 + 6XYZ,
+    PAPER:515-517).  On walked schemes with an asymmetric type, f equals the sum of the
+    type polynomials of the six schemes the meta operators produce from the scheme --
+    rotations (cyclic (x,y,z)) and rotations of its transpose (a transposition) generate
+    S_3 (R25/R26) -- and f is unchanged by those operators."""
+    m, n, p, c = load_scheme("sec36_after.txt")
+    assert orc.sym_invariant(m, n, p, c) == {(2, 2, 2): 6, (1, 1, 1): 36}
+    asym = 0
+    for fmt, seed in [((2, 3, 4), 3), ((3, 3, 3), 5), ((2, 2, 3), 9), ((3, 4, 2), 11)]:
+        w = orc.walker(*fmt, 0, 32, walker_id=seed)
+        w.seed_naive()
+        w.walk(6000, seed)
+        s = w.rows()
+        f = orc.sym_invariant(*fmt, s)
+        assert sum(f.values()) == 6 * s.shape[0]
+        orbit = []
+        for start in [(fmt, s), orc.meta("transpose", fmt, s)]:
+            cur = start
+            for _ in range(3):
+                orbit.append(cur)
+                cur = orc.meta("rotate", *cur)
+        acc = {}
+        for g_fmt, g_s in orbit:
+            _add(acc, orc.type_invariant(*g_fmt, g_s))
+            assert orc.sym_invariant(*g_fmt, g_s) == f
+        assert acc == f, fmt
+        t = orc.type_invariant(*fmt, s)
+        asym += any(t.get((b, a, cc), 0) != v for (a, b, cc), v in t.items())
+    assert asym >= 1        # the pin saw a scheme whose type polynomial is not symmetric
+
+
 def test_matrix_rank_vs_numpy(orc):
     rng = np.random.default_rng(7)
     for _ in range(300):
