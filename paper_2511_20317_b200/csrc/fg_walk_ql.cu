@@ -4,44 +4,50 @@
 //
 // Why: walk_q4 keeps one class mask per row and role (R bits); at R = 96 that is 3.4 KB
 // per walker and 8 walkers per warp would not fit shared memory.  Here every row keeps,
-// per role, the next and the previous row of its class in row order (bytes), which is
-// all R10/R11 need: the t-th later member of row i is t+1 `next` hops, and the later
-// count of a row (the length of its `next` chain) is kept explicitly.  A class change
-// finds the new class with one compare pass over the rows (split over the quad) and
-// splices the row in; leaving a class relinks the neighbours and walks the `prev`
-// chain to decrement the later counts below.
+// per role, the next row of its class in row order (bytes), which is all R10/R11 need:
+// the t-th later member of row i is t+1 `next` hops, and the later count of a row (the
+// length of its `next` chain) is kept explicitly.  A class change is ONE compare pass over
+// the rows (split over the quad) against the old and the new key: it gives the old and
+// the new neighbours, the members below the row (whose later counts change) and the
+// candidate-pair totals, so no `prev` links are stored.  Five words per row (three keys,
+// next links + W sign, later counts) put the C3 population (16384 walkers) in one wave
+// of 2-warp CTAs (14 warps per SM).
 //
 // Per walker (shared memory, per warp stride 8 as in walk_q4; lane q owns rows l % 4 == q):
 //   F(l,X)  row l's factor X key (W up to sign; the sign is bit 24 of NX(l))
 //   NX(l)   next row of l's U / V / W class (bytes 0..2, 0xFF = none)
-//   PV(l)   previous row, same packing
 //   L(l)    later counts, 3 x 10 bits
 //   G(g)    later counts before row group g (8 rows): word 0 = U | V << 16, word 1 = W
-// The best scheme lives in HBM (written on acceptance).
+// R15 (reduce_all) searches partners of the rows in a dirty set D only: flips are cleaned
+// by R12, so only rows changed by expands (or global merges) since the last clean scan
+// can be in a reducible pair (as in fg_walk_wl.cuh); D overflow or a fresh load falls
+// back to the full lexicographic scan.  The best scheme lives in HBM (written on
+// acceptance; rows up to the previous best rank only).
 //
 // Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
-// tests/test_gpu_kernels.py.
+// tests/test_gpu_kernels.py, tests/test_gpu_fuzz.py, tests/test_gpu_fullsize.py.
 #include <cstdlib>
 #include <type_traits>
 #include "fg_device.cuh"
 
 using namespace fgd;
 
-#define QL_THREADS 32
+#define QL_THREADS 64                  // 2-warp CTAs: one 1 KB CTA reserve per 2 warps
+#define QL_MINB 7
 
 namespace {
 
 constexpr int NIL = 0xFF;
 
 template <class P, int NWD>
-__global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
+__global__ void __launch_bounds__(QL_THREADS, QL_MINB) walk_ql(WalkArgs a)
 {
     typedef typename P::F F;
     static_assert(sizeof(F) == 4, "one-word factor layouts only");
     constexpr int RM = 32 * NWD;                 // row capacity of this instantiation
     constexpr int NG = RM / 8;                   // row groups of the prefix
-    constexpr int S_NX = 3 * RM, S_PV = 4 * RM, S_L = 5 * RM, S_G = 6 * RM;
-    constexpr int SLOTS = 6 * RM + 2 * NG;
+    constexpr int S_NX = 3 * RM, S_L = 4 * RM, S_G = 5 * RM;
+    constexpr int SLOTS = 5 * RM + 2 * NG;
     extern __shared__ uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int q = lane & 3;
@@ -78,7 +84,6 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
 
 #define FK(l, X) S[(3 * (l) + (X)) * 8]
 #define NXW(l) S[(S_NX + (l)) * 8]
-#define PVW(l) S[(S_PV + (l)) * 8]
 #define LK(l) S[(S_L + (l)) * 8]
 #define GK(g, h) S[(S_G + 2 * (g) + (h)) * 8]
 
@@ -86,7 +91,6 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     auto qsync = [&]() __attribute__((always_inline)) { __syncwarp(qm); };
     auto byte_of = [](uint32_t w, int X) __attribute__((always_inline)) -> int { return (int)((w >> (8 * X)) & 0xFFu); };
     auto nxt = [&](int l, int X) __attribute__((always_inline)) -> int { return byte_of(NXW(l), X); };
-    auto prv = [&](int l, int X) __attribute__((always_inline)) -> int { return byte_of(PVW(l), X); };
     auto set_byte = [](uint32_t w, int X, int v) __attribute__((always_inline)) -> uint32_t {
         return (w & ~(0xFFu << (8 * X))) | (((uint32_t)v & 0xFFu) << (8 * X));
     };
@@ -125,8 +129,11 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     // restores the shared-memory image and scalars the previous chunk saved (ql_img)
     int nnz_cur = 0;
     uint32_t nCU = 0, nCV = 0, nCW = 0;     // flip-candidate pairs per role (R10)
-    bool maybe = true;                      // R15: a full reduce_all may find work
-    constexpr int IMG = SLOTS + 5;          // image words per walker
+    // R15 dirty set D (<= 6 rows, 8 bits each) and its overflow flag (fresh load: any pair)
+    uint64_t dset = 0;
+    int nD = 0;
+    bool dover = true;
+    constexpr int IMG = SLOTS + 7;          // image words per walker
     uint32_t *const img = a.ql_img ? a.ql_img + (size_t)wk * IMG : nullptr;
     const bool resume = chunk > 0 && img != nullptr && valid;
     if (resume) {
@@ -134,7 +141,9 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         for (int k = q; k < SLOTS; k += 4) S[k * 8] = img[k];
         nnz_cur = (int)img[SLOTS];
         nCU = img[SLOTS + 1]; nCV = img[SLOTS + 2]; nCW = img[SLOTS + 3];
-        maybe = img[SLOTS + 4] != 0u;
+        dset = (uint64_t)img[SLOTS + 4] | ((uint64_t)img[SLOTS + 5] << 32);
+        nD = (int)(img[SLOTS + 6] & 0xFFu);
+        dover = (img[SLOTS + 6] >> 8) != 0u;
         qsync();
     }
     uint32_t own_sign = 0;                       // W signs of own rows (bit l / 4)
@@ -166,23 +175,22 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         uint32_t pu = 0, pv_ = 0, pw = 0;
 #pragma unroll 1
         for (int l = q; l < RM; l += 4) {
-            uint32_t nxw = 0xFFFFFFu, pvw = 0xFFFFFFu, lc = 0;
+            uint32_t nxw = 0xFFFFFFu, lc = 0;
             if (l < r) {
 #pragma unroll 1
                 for (int X = 0; X < 3; ++X) {
                     const uint32_t key = FK(l, X);
-                    int nx = NIL, pv = NIL, cnt = 0;
-                    for (int j = 0; j < r; ++j) {
-                        if (j == l || FK(j, X) != key) continue;
-                        if (j < l) pv = j;
-                        else { if (nx == NIL) nx = j; cnt++; }
+                    int nx = NIL, cnt = 0;
+                    for (int j = l + 1; j < r; ++j) {
+                        if (FK(j, X) != key) continue;
+                        if (nx == NIL) nx = j;
+                        cnt++;
                     }
                     nxw = set_byte(nxw, X, nx);
-                    pvw = set_byte(pvw, X, pv);
                     lc |= (uint32_t)cnt << (10 * X);
                 }
             }
-            NXW(l) = nxw | (((own_sign >> (l >> 2)) & 1u) << 24); PVW(l) = pvw; LK(l) = lc;
+            NXW(l) = nxw | (((own_sign >> (l >> 2)) & 1u) << 24); LK(l) = lc;
             pu += lc & 1023u; pv_ += (lc >> 10) & 1023u; pw += lc >> 20;
         }
         pu += __shfl_xor_sync(qm, pu, 1); pu += __shfl_xor_sync(qm, pu, 2);
@@ -207,26 +215,28 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     auto row_zero = [&](int l) __attribute__((always_inline)) -> bool { return P::zero(FK(l, 0)) || P::zero(FK(l, 1)) || P::zero(FK(l, 2)); };
 
     // ---- class structure primitives ----
-    // leave row l's X class: neighbours relinked, the rows below l lose a later member.
-    // Writes by owners; the caller syncs before the next cross-lane read.
-    auto unlink_role = [&](int l, int X) __attribute__((always_inline)) {
-        const int p = prv(l, X), n = nxt(l, X);
-        const uint32_t lx = (LK(l) >> (10 * X)) & 1023u;
-        int below = 0;
-        for (int m = p; m != NIL; m = prv(m, X)) {
-            if (owner(m)) LK(m) -= 1u << (10 * X);
-            below++;
+    // rows j (live, != l) of mask word w whose role-X key equals `key`: each lane compares
+    // its 8 rows, the quad ORs the four parts (replicated in the quad).  Collective over msk.
+    auto cmask = [&](int w, int X, uint32_t key, int l, unsigned msk) __attribute__((always_inline)) -> uint32_t {
+        uint32_t mw = 0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            const int j = 32 * w + 4 * kk + q;
+            mw |= (FK(j, X) == key) ? (1u << (4 * kk + q)) : 0u;
         }
-        if (p != NIL && owner(p)) NXW(p) = set_byte(NXW(p), X, n);
-        if (n != NIL && owner(n)) PVW(n) = set_byte(PVW(n), X, p);
-        addn(X, -(below + (int)lx));
+        mw |= __shfl_xor_sync(msk, mw, 1);
+        mw |= __shfl_xor_sync(msk, mw, 2);
+        return mw & live_in(w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
     };
-    // join the class of `key` in role X (FK(l,X) already holds key, written by owner(l)):
-    // one compare pass over the rows, split over the quad.  Collective over msk.
-    // With WARP it also reports whether some row other than l and `excl` shares two factors
-    // with row l after the change (R12's skip test): the same pass compares the rows with
-    // l's other two class keys.
-    auto link_role = [&](auto wtag, int l, int X, uint32_t key, bool act, int excl, bool &two) __attribute__((always_inline)) {
+    // Row l's X key goes from `okey` to `key` (fresh: l was in no X class): ONE compare
+    // pass against both keys gives the old neighbours (pO, sO: relinked), the new ones
+    // (pK, sK: l spliced in), the members below l (their later counts lose / gain l) and
+    // the change of the role's pair count.  With WARP the same pass also reports whether
+    // some row other than l and `excl` shares two factors with row l after the change
+    // (R12's skip test: rows compared with l's other two keys).  Writes by owners; the
+    // caller syncs before the next cross-lane read.
+    auto change_class = [&](auto wtag, int l, int X, uint32_t okey, uint32_t key, bool fresh, bool act, int excl,
+                            bool &two) __attribute__((always_inline)) {
         constexpr bool WARP = decltype(wtag)::value;
         const unsigned msk = WARP ? FULL : qm;
         const int O1 = X == 2 ? 0 : X + 1, O2 = X == 0 ? 2 : X - 1;
@@ -234,19 +244,24 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         two = false;
         // one mask word (32 rows) per iteration, not unrolled: a compact loop body keeps
         // the instruction stream small (the unrolled 24-row pass missed the i-cache)
-        int pred = NIL, succ = NIL, nab = 0, tot = 0;
+        int pO = NIL, sO = NIL, pK = NIL, sK = NIL, nab = 0, tot = 0;
 #pragma unroll 1
         for (int w = 0; w < NWD; ++w) {
-            uint32_t mw = 0;
+            uint32_t mk = 0, mo = 0;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {
                 const int j = 32 * w + 4 * kk + q;
-                mw |= (FK(j, X) == key) ? (1u << (4 * kk + q)) : 0u;
+                const uint32_t fj = FK(j, X);
+                mk |= (fj == key) ? (1u << (4 * kk + q)) : 0u;
+                mo |= (fj == okey) ? (1u << (4 * kk + q)) : 0u;
             }
-            mw |= __shfl_xor_sync(msk, mw, 1);
-            mw |= __shfl_xor_sync(msk, mw, 2);
+            mk |= __shfl_xor_sync(msk, mk, 1);
+            mo |= __shfl_xor_sync(msk, mo, 1);
+            mk |= __shfl_xor_sync(msk, mk, 2);
+            mo |= __shfl_xor_sync(msk, mo, 2);
             const uint32_t keep = live_in(w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
-            mw &= keep;
+            mk &= keep;
+            mo &= fresh ? 0u : keep;
             if (WARP) {
                 uint32_t m1 = 0, m2 = 0;
 #pragma unroll
@@ -260,59 +275,51 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
                 m1 |= __shfl_xor_sync(msk, m1, 2);
                 m2 |= __shfl_xor_sync(msk, m2, 2);
                 const uint32_t ex = ((excl >> 5) == w && excl >= 0) ? (1u << (excl & 31)) : 0u;
-                const uint32_t k = keep & ~ex;
-                two = two || ((((mw & (m1 | m2)) | (m1 & m2)) & k) != 0u);
+                two = two || ((((mk & (m1 | m2)) | (m1 & m2)) & keep & ~ex) != 0u);
             }
             if (act) {
-                const uint32_t lo = mw & below_in(l, w), hi = mw & above_in(l, w);
-                if (lo) pred = 32 * w + 31 - __clz(lo);
-                if (hi && succ == NIL) succ = 32 * w + __ffs(hi) - 1;
+                const uint32_t bl = below_in(l, w), ab = above_in(l, w);
+                const uint32_t lo = mk & bl, hi = mk & ab, olo = mo & bl, ohi = mo & ab;
+                if (lo) pK = 32 * w + 31 - __clz(lo);
+                if (hi && sK == NIL) sK = 32 * w + __ffs(hi) - 1;
+                if (olo) pO = 32 * w + 31 - __clz(olo);
+                if (ohi && sO == NIL) sO = 32 * w + __ffs(ohi) - 1;
                 nab += __popc(hi);
-                tot += __popc(mw);
-                for (uint32_t t = lo & (0x11111111u << q); t; t &= t - 1u) {
-                    const int m = 32 * w + __ffs(t) - 1;
-                    LK(m) += 1u << (10 * X);
-                }
+                tot += __popc(mk) - __popc(mo);
+                const uint32_t own = 0x11111111u << q;
+                for (uint32_t t = lo & ~olo & own; t; t &= t - 1u) LK(32 * w + __ffs(t) - 1) += 1u << (10 * X);
+                for (uint32_t t = olo & ~lo & own; t; t &= t - 1u) LK(32 * w + __ffs(t) - 1) -= 1u << (10 * X);
             }
         }
         if (!act) return;
         if (owner(l)) {
-            NXW(l) = set_byte(NXW(l), X, succ);
-            PVW(l) = set_byte(PVW(l), X, pred);
+            FK(l, X) = key;
+            NXW(l) = set_byte(NXW(l), X, sK);
             LK(l) = (LK(l) & ~(1023u << (10 * X))) | ((uint32_t)nab << (10 * X));
         }
-        if (pred != NIL && owner(pred)) NXW(pred) = set_byte(NXW(pred), X, l);
-        if (succ != NIL && owner(succ)) PVW(succ) = set_byte(PVW(succ), X, l);
+        if (pO != NIL && owner(pO)) NXW(pO) = set_byte(NXW(pO), X, sO);
+        if (pK != NIL && owner(pK)) NXW(pK) = set_byte(NXW(pK), X, l);
         addn(X, tot);
-    };
-    // row l's X key becomes `key` (fresh: l is in no X class yet).  Collective over the
-    // quad (wtag false) or the warp (wtag true: every quad calls it, `act` gates it).
-    auto set_class = [&](auto wtag, int l, int X, uint32_t key, bool fresh, bool act, int excl, bool &two) __attribute__((always_inline)) {
-        constexpr bool WARP = decltype(wtag)::value;
-        const unsigned msk = WARP ? FULL : qm;
-        if (act && !fresh) unlink_role(l, X);
-        __syncwarp(msk);
-        if (act && owner(l)) FK(l, X) = key;
-        link_role(wtag, l, X, key, act, excl, two);
-        __syncwarp(msk);
     };
     // store a whole (normalised) row; only changed keys pay a class update.  Quad.
     auto write_row = [&](int l, const Row<P> &x, bool fresh) __attribute__((always_inline)) {
         const F o0 = FK(l, 0), o1 = FK(l, 1), o2 = FK(l, 2);
         if (fresh) {
             qsync();
-            if (owner(l)) LK(l) = 0;
+            if (owner(l)) { LK(l) = 0; NXW(l) = 0xFFFFFFu; }
         } else {
             nnz_cur -= P::popd(o0) + P::popd(o1) + P::popd(o2);
         }
         nnz_cur += P::popd(x.u) + P::popd(x.v) + P::popd(x.w);
+        qsync();
         // one inlined class update, looped over the roles (rare path: code size)
 #pragma unroll 1
         for (int X = 0; X < 3; ++X) {
             const F kX = X == 0 ? x.u : (X == 1 ? x.v : P::abs(x.w));
             const F oX = X == 0 ? o0 : (X == 1 ? o1 : o2);
             bool dummy;
-            if (fresh || kX != oX) set_class(std::false_type{}, l, X, kX, fresh, true, -1, dummy);
+            if (fresh || kX != oX) change_class(std::false_type{}, l, X, oX, kX, fresh, true, -1, dummy);
+            qsync();
         }
         set_wbit(l, P::first_neg(x.w));
         qsync();
@@ -327,23 +334,37 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             nnz_cur += P::popd(val) - P::popd(old);
             set_wbit(l, Y == 2 ? (uint32_t)fn : (wbit(l) ^ (uint32_t)fn));
         }
-        set_class(std::true_type{}, l, Y, key, false, act && key != old, excl, two);
+        change_class(std::true_type{}, l, Y, old, key, false, act && key != old, excl, two);
+        __syncwarp();
     };
-    // rows j (> lmin) sharing two factors with row l, as a row mask
+    // rows j (live, != l, > lmin) sharing two factor keys with row l (W up to sign), as a
+    // row mask: one compare pass (quad)
     auto two_mask = [&](int l, int lmin, uint32_t (&cm)[NWD]) {
+        const uint32_t u = FK(l, 0), v = FK(l, 1), w_ = FK(l, 2);
 #pragma unroll
-        for (int w = 0; w < NWD; ++w) cm[w] = 0;
-        const F v = FK(l, 1), w_ = FK(l, 2);
-        auto add = [&](int m) __attribute__((always_inline)) {
-            if (m <= lmin) return;
+        for (int w = 0; w < NWD; ++w) {
+            uint32_t m0 = 0, m1 = 0, m2 = 0;
 #pragma unroll
-            for (int w = 0; w < NWD; ++w)
-                if ((m >> 5) == w) cm[w] |= 1u << (m & 31);
-        };
-        for (int m = nxt(l, 0); m != NIL; m = nxt(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w_) add(m);
-        for (int m = prv(l, 0); m != NIL; m = prv(m, 0)) if (FK(m, 1) == v || FK(m, 2) == w_) add(m);
-        for (int m = nxt(l, 1); m != NIL; m = nxt(m, 1)) if (FK(m, 2) == w_) add(m);
-        for (int m = prv(l, 1); m != NIL; m = prv(m, 1)) if (FK(m, 2) == w_) add(m);
+            for (int kk = 0; kk < 8; ++kk) {
+                const int j = 32 * w + 4 * kk + q;
+                const uint32_t bit = 1u << (4 * kk + q);
+                m0 |= FK(j, 0) == u ? bit : 0u;
+                m1 |= FK(j, 1) == v ? bit : 0u;
+                m2 |= FK(j, 2) == w_ ? bit : 0u;
+            }
+            uint32_t m = (m0 & m1) | (m0 & m2) | (m1 & m2);
+            m |= __shfl_xor_sync(qm, m, 1);
+            m |= __shfl_xor_sync(qm, m, 2);
+            cm[w] = m & live_in(w) & above_in(lmin, w) & ~(((l >> 5) == w) ? (1u << (l & 31)) : 0u);
+        }
+    };
+    auto d_add = [&](int x) __attribute__((always_inline)) {
+        if (dover) return;
+        for (int k = 0; k < nD; ++k)
+            if ((int)((dset >> (8 * k)) & 0xFFu) == x) return;
+        if (nD == 6) { dover = true; return; }
+        dset |= (uint64_t)x << (8 * nD);
+        nD++;
     };
 
     // R14 remove(h) with the 2-entry worklist (entries == h dropped, r-1 -> h).  Quad.
@@ -354,44 +375,73 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         if (nwl >= 2 && wl1 != h) { if (n2 == 0) x0 = wl1; else x1 = wl1; n2++; }
         wl0 = x0; wl1 = x1; nwl = n2;
         nnz_cur -= P::popd(FK(h, 0)) + P::popd(FK(h, 1)) + P::popd(FK(h, 2));
+        // h leaves its classes: its neighbours are relinked, the members below it lose a
+        // later member (F(h) keeps the old keys until overwritten; the moves exclude h)
 #pragma unroll 1
         for (int X = 0; X < 3; ++X) {
-            unlink_role(h, X);
+            const uint32_t o = FK(h, X);
+            int pO = NIL, sO = NIL, tot = 0;
+#pragma unroll 1
+            for (int w = 0; w < NWD; ++w) {
+                const uint32_t m = cmask(w, X, o, h, qm);
+                const uint32_t lo = m & below_in(h, w), hi = m & above_in(h, w);
+                if (lo) pO = 32 * w + 31 - __clz(lo);
+                if (hi && sO == NIL) sO = 32 * w + __ffs(hi) - 1;
+                tot += __popc(m);
+                for (uint32_t t = lo & (0x11111111u << q); t; t &= t - 1u) LK(32 * w + __ffs(t) - 1) -= 1u << (10 * X);
+            }
+            if (pO != NIL && owner(pO)) NXW(pO) = set_byte(NXW(pO), X, sO);
+            addn(X, -tot);
             qsync();
         }
         if (h != last) {
             // row `last` (the largest live index: the tail of each of its classes) moves
             // to h: in each class it moves down past its members in (h, last), which lose
-            // it as a later member; pred / succ = its new neighbours
+            // it as a later member; pred / succ = its new neighbours, and the member that
+            // pointed to it becomes a tail if it lies above h
             const F k0 = FK(last, 0), k1 = FK(last, 1), k2 = FK(last, 2);
-            uint32_t nxw = 0xFFFFFFu, pvw = 0xFFFFFFu, lc = 0;
+            uint32_t nxw = 0xFFFFFFu, lc = 0;
 #pragma unroll 1
             for (int X = 0; X < 3; ++X) {
-                const int p1 = prv(last, X);
-                int succ = NIL, cnt = 0, m = p1;
-                for (; m != NIL && m > h; m = prv(m, X)) {
-                    if (owner(m)) LK(m) -= 1u << (10 * X);
-                    succ = m;
-                    cnt++;
+                const uint32_t key = X == 0 ? k0 : (X == 1 ? k1 : k2);
+                int pred = NIL, succ = NIL, tail = NIL, nab = 0;
+#pragma unroll 1
+                for (int w = 0; w < NWD; ++w) {
+                    const uint32_t m = cmask(w, X, key, last, qm) & ~(((h >> 5) == w) ? (1u << (h & 31)) : 0u);
+                    const uint32_t lo = m & below_in(h, w), hi = m & above_in(h, w);
+                    if (lo) pred = 32 * w + 31 - __clz(lo);
+                    if (hi && succ == NIL) succ = 32 * w + __ffs(hi) - 1;
+                    if (m) tail = 32 * w + 31 - __clz(m);
+                    nab += __popc(hi);
+                    for (uint32_t t = hi & (0x11111111u << q); t; t &= t - 1u) LK(32 * w + __ffs(t) - 1) -= 1u << (10 * X);
                 }
-                const int pred = m;
-                qsync();
-                if (p1 != NIL && p1 > h && owner(p1)) NXW(p1) = set_byte(NXW(p1), X, NIL);
+                if (tail != NIL && tail > h && owner(tail)) NXW(tail) = set_byte(NXW(tail), X, NIL);
                 if (pred != NIL && owner(pred)) NXW(pred) = set_byte(NXW(pred), X, h);
-                if (succ != NIL && owner(succ)) PVW(succ) = set_byte(PVW(succ), X, h);
                 nxw = set_byte(nxw, X, succ);
-                pvw = set_byte(pvw, X, pred);
-                lc |= (uint32_t)cnt << (10 * X);
+                lc |= (uint32_t)nab << (10 * X);
                 qsync();
             }
             const uint32_t sl = wbit(last);
+            qsync();
             if (owner(h)) {
                 FK(h, 0) = k0; FK(h, 1) = k1; FK(h, 2) = k2;
-                NXW(h) = nxw | (sl << 24); PVW(h) = pvw; LK(h) = lc;
+                NXW(h) = nxw | (sl << 24); LK(h) = lc;
             }
             if (nwl >= 1 && wl0 == last) wl0 = h;
             if (nwl >= 2 && wl1 == last) wl1 = h;
         }
+        // D: entries == h dropped, last -> h
+        uint64_t nd = 0;
+        int nn = 0;
+        for (int k = 0; k < nD; ++k) {
+            int x = (int)((dset >> (8 * k)) & 0xFFu);
+            if (x == h) continue;
+            if (x == last) x = h;
+            nd |= (uint64_t)x << (8 * nn);
+            nn++;
+        }
+        dset = nd;
+        nD = nn;
         if (owner(last)) LK(last) = 0;
         r--;
         qsync();
@@ -420,9 +470,39 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             } else {
                 for (int l = 0; l < r; ++l)
                     if (row_zero(l)) { rm0 = l; break; }
-                if (rm0 >= 0) c_zero++; else { ib = 0; ie = r; }
+                // full lexicographic scan only after a load or a D overflow
+                if (rm0 >= 0) c_zero++; else if (dover) { ib = 0; ie = r; }
             }
-            if (rm0 < 0) {
+            if (rm0 < 0 && !local && !dover) {
+                // R15 over D: the lexicographically first reducible pair involving a dirty
+                // row (for a dirty d the first partner j in row order gives its first pair)
+                int bk = 0x7fffffff;
+#pragma unroll 1
+                for (int k = 0; k < nD; ++k) {
+                    const int d = (int)((dset >> (8 * k)) & 0xFFu);
+                    uint32_t cm[NWD];
+                    two_mask(d, -1, cm);
+                    const Row<P> rd = read_row(d);
+                    bool found = false;
+#pragma unroll
+                    for (int w = 0; w < NWD; ++w)
+                        for (uint32_t c = cm[w]; c && !found; c &= c - 1u) {
+                            const int j = 32 * w + __ffs(c) - 1;
+                            Row<P> tmp;
+                            if (!reducible<P>(rd, read_row(j), tmp)) continue;
+                            found = true;
+                            const int kk = (j < d ? j : d) * 256 + (j < d ? d : j);
+                            bk = kk < bk ? kk : bk;
+                        }
+                }
+                if (bk == 0x7fffffff) break;
+                lo = bk >> 8;
+                wr = lo;
+                rm0 = bk & 255;
+                reducible<P>(read_row(lo), read_row(rm0), merged);     // row i as base (R15)
+                c_merge++;
+                if (has_zero(merged)) { rm1 = lo; c_zero++; }
+            } else if (rm0 < 0) {
                 // the first (i, j) in (i, j) order with reducible(row i, row j): local over
                 // all j != t, global over j > i (R12 / R15); one inlined search
 #pragma unroll 1
@@ -454,6 +534,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
                 if (h < 0) break;
                 remove_row(h, wl0, wl1, nwl);
             }
+            if (!local && wr >= 0 && rm1 < 0) d_add(lo);       // the merged row (R15) is dirty
             if (push) {
                 wl1 = wl0;
                 wl0 = lo;
@@ -519,14 +600,15 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             x.v = t == 0 ? ri.v : (t == 1 ? rj.v : rn.v);
             x.w = t == 0 ? ri.w : (t == 1 ? rj.w : rn.w);
             write_row(l, x, t == 2);
+            d_add(l);
         }
-        maybe = true;
         return true;
     };
 
     // store the current rows in plane layout (own rows; zeros above r up to R)
-    auto store_rows = [&](uint64_t *dst) __attribute__((always_inline)) {
-        for (int l = q; l < R; l += 4) {
+    // rows l < n (n >= r; zeros for r <= l < n)
+    auto store_rows = [&](uint64_t *dst, int n) __attribute__((always_inline)) {
+        for (int l = q; l < n; l += 4) {
             const bool lv = l < r;
             const F u = lv ? FK(l, 0) : 0, v = lv ? FK(l, 1) : 0, w = lv ? fac(l, 2) : 0;
             dst[0 * R + l] = P::dig(u); dst[1 * R + l] = P::sgn(u);
@@ -540,7 +622,7 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         if (q == 0) slot = atomicAdd(a.q_count, 1u);
         slot = __shfl_sync(qm, slot, qb);
         if (slot < a.q_cap) {
-            store_rows(a.q_planes + (size_t)slot * FG_PLANES * R);
+            store_rows(a.q_planes + (size_t)slot * FG_PLANES * R, r);   // the verifier reads rank rows
             if (q == 0) {
                 fg_qmeta qm_;
                 qm_.walker = wk; qm_.step = step; qm_.rank = r; qm_.ok = -1;
@@ -700,16 +782,17 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
             const bool need_local = P::zero(e_ny) || P::zero(e_nz) || two_ab || same >= 2;
 #pragma unroll 1
             for (int ph = 0; ph < 2; ++ph) {
-                const bool run = ph == 0 ? need_local : ((bern & 2u) && maybe);
+                const bool run = ph == 0 ? need_local : ((bern & 2u) && (dover || nD > 0));
                 if (run) reduce_rows(ph == 0, alpha, beta);
                 if (ph == 0) {
                     const bool strict = r < best;
                     if (strict || (r == best && (bern & 1u))) {
+                        // rows >= the previous best rank are already zero in HBM
+                        store_rows(bw, best);
                         best = r;
                         best_adds = nnz_cur - 2 * r - a.mp;
                         c_copy++;
                         flags |= 4u;
-                        store_rows(bw);
                         if (strict) {
                             flags |= 8u;
                             c_impr++;
@@ -721,7 +804,9 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
                         flags |= 16u;
                     }
                 } else if (run) {
-                    maybe = false;
+                    dset = 0;                   // reduce_all ran to completion: clean
+                    nD = 0;
+                    dover = false;
                 }
             }
             // ---- PAPER:319-321 expand ----
@@ -747,14 +832,17 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         if (q == 0) {
             img[SLOTS] = (uint32_t)nnz_cur;
             img[SLOTS + 1] = nCU; img[SLOTS + 2] = nCV; img[SLOTS + 3] = nCW;
-            img[SLOTS + 4] = maybe ? 1u : 0u;
+            img[SLOTS + 4] = (uint32_t)dset; img[SLOTS + 5] = (uint32_t)(dset >> 32);
+            img[SLOTS + 6] = (uint32_t)nD | (dover ? 0x100u : 0u);
         }
     }
-    // ---------------- store own rows; best additions from the best rows in HBM ----------------
+    // ---------------- last chunk: store own rows; best additions from the best rows ----------------
+    // (earlier chunks hand the state over in the image only)
     __syncwarp();
-    if (valid) store_rows(a.cur + (size_t)wk * FG_PLANES * R);
+    const bool last_chunk = chunk + 1 >= a.chunks;
+    if (valid && last_chunk) store_rows(a.cur + (size_t)wk * FG_PLANES * R, R);
     int best_nnz = 0;
-    for (int l = q; l < R && valid; l += 4)
+    for (int l = q; l < R && valid && last_chunk; l += 4)
         if (l < best) best_nnz += __popcll(bw[0 * R + l]) + __popcll(bw[2 * R + l]) + __popcll(bw[4 * R + l]);
     best_nnz += __shfl_xor_sync(qm, best_nnz, 1);
     best_nnz += __shfl_xor_sync(qm, best_nnz, 2);
@@ -777,8 +865,9 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
         hp->cnt[FG_CNT_REDUCE_CALLS] += c_red;
         int adds = best_nnz - 2 * best - a.mp;
         if (adds < 0) adds = 0;
-        atomicMin(a.best_key, ((unsigned long long)best << 54) | ((unsigned long long)adds << 36) |
-                                  (unsigned long long)wk);
+        if (last_chunk)
+            atomicMin(a.best_key, ((unsigned long long)best << 54) | ((unsigned long long)adds << 36) |
+                                      (unsigned long long)wk);
     }
     // this group's chunk is stored: release the next chunk
     __syncwarp();
@@ -788,7 +877,6 @@ __global__ void __launch_bounds__(QL_THREADS) walk_ql(WalkArgs a)
     }   // task loop
 #undef FK
 #undef NXW
-#undef PVW
 #undef LK
 #undef GK
 }
@@ -797,7 +885,7 @@ template <class P, int NWD>
 cudaError_t launch_ql(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     constexpr int RM = 32 * NWD;
-    const size_t smem = (size_t)(6 * RM + 2 * (RM / 8)) * 8 * 4 * (QL_THREADS / 32);
+    const size_t smem = (size_t)(5 * RM + 2 * (RM / 8)) * 8 * 4 * (QL_THREADS / 32);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(walk_ql<P, NWD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -808,7 +896,7 @@ cudaError_t launch_ql(const WalkArgs &a, int num_sms, cudaStream_t st)
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_ql<P, NWD>, QL_THREADS, smem);
     if (e != cudaSuccess) return e;
     if (bps < 1) bps = 1;
-    const int64_t resident = (int64_t)num_sms * bps;            // warps (1-warp CTAs)
+    const int64_t resident = (int64_t)num_sms * bps * (QL_THREADS / 32);   // warps
     const int64_t groups = (a.num_walkers + 7) / 8;
     WalkArgs b = a;
     // one wave: one task per warp; more: 8 step chunks per group over persistent warps
@@ -819,7 +907,8 @@ cudaError_t launch_ql(const WalkArgs &a, int num_sms, cudaStream_t st)
     }
     if ((uint64_t)b.chunks > a.steps) b.chunks = a.steps > 0 ? (uint32_t)a.steps : 1u;
     b.chunk_steps = (a.steps + b.chunks - 1) / b.chunks;
-    const int64_t blocks = groups < resident ? groups : resident;
+    const int64_t warps = groups < resident ? groups : resident;
+    const int64_t blocks = (warps + QL_THREADS / 32 - 1) / (QL_THREADS / 32);
     walk_ql<P, NWD><<<(unsigned)blocks, QL_THREADS, smem, st>>>(b);
     return cudaGetLastError();
 }

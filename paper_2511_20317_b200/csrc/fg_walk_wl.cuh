@@ -695,7 +695,10 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                 int pO0 = NIL, sO0 = NIL, pK0 = NIL, sK0 = NIL, aK0 = 0, tD0 = 0;
                 int pO1 = NIL, sO1 = NIL, pK1 = NIL, sK1 = NIL, aK1 = 0, tD1 = 0;
                 bool hit = false;
-#pragma unroll 1
+                // two words per iteration for the 16-byte layouts (ILP at ~2 resident warps
+                // per scheduler: +2 % on C5); one for P32 (-2 % on C4, scripts/gpu_r02_ab.sh)
+                constexpr int PASS_UNROLL = sizeof(F) > 8 ? 2 : 1;
+#pragma unroll PASS_UNROLL
                 for (int w = 0; w < nwd; ++w) {
                     const int l = 32 * w + lane;
                     const F xX = pX[l], xY = pY[l], xZ = pZ[l];
