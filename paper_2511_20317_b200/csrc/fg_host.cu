@@ -601,9 +601,12 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         verified += std::min(hm.q_count, c->qcap);
         remaining -= chunk;
     } while (remaining > 0);
-    if (a.dbg && hm.dbgbuf[0])
+    if (a.dbg && hm.dbgbuf[0]) {
+        // FG_DBG structure self-check failed: report and fail the call
         fprintf(stderr, "libfg dbg: %u %u %u %u %u %u %u %u %u %u\n", hm.dbgbuf[0], hm.dbgbuf[1], hm.dbgbuf[2],
                 hm.dbgbuf[3], hm.dbgbuf[4], hm.dbgbuf[5], hm.dbgbuf[6], hm.dbgbuf[7], hm.dbgbuf[8], hm.dbgbuf[9]);
+        return FG_E_STATE;
+    }
     if (hm.q_overflow) {
         // strict improvements that missed the queue: verify those walkers' final bests
         CK(cudaMemsetAsync(&c->d_misc->restarted, 0, sizeof(unsigned long long), c->stream));

@@ -15,7 +15,9 @@ orc = Oracle()
 cases = [((5, 5, 5), 0, 160, 64, 3000), ((6, 7, 9), 0, 416, 16, 1500), ((4, 5, 12), 1, 256, 32, 2000),
          ((5, 5, 5), 0, 160, 64, 300), ((4, 4, 4), 0, 96, 64, 600), ((3, 3, 3), 0, 40, 64, 1500),
          ((4, 5, 12), 0, 256, 32, 200), ((4, 5, 12), 1, 256, 32, 200), ((6, 7, 9), 0, 416, 16, 150),
-         ((4, 4, 4), 1, 160, 32, 500), ((2, 3, 4), 0, 64, 64, 2000)]
+         ((4, 4, 4), 1, 160, 32, 500), ((2, 3, 4), 0, 64, 64, 2000),
+         ((2, 2, 16), 0, 96, 64, 2000), ((2, 3, 20), 0, 160, 32, 1500), ((1, 1, 40), 0, 64, 32, 1500),
+         ((1, 2, 30), 1, 96, 32, 1500)]
 only = sys.argv[1:] and int(sys.argv[1])
 st = torch.cuda.current_stream().cuda_stream
 bad = 0

@@ -205,3 +205,26 @@ def test_wm_forced_for_wide(fg, orc, case):
     ids = sample_walkers(W, 8, seed=R)
     ref = orc.run_walkers(m, n, p, ring, R, 0, 0, steps, seed, ids=ids)
     _check(got, ref, ids)
+
+
+@pytest.mark.parametrize("case", [((2, 2, 16), ZT, 96, 70, 2500), ((2, 3, 20), ZT, 160, 50, 1500),
+                                  ((1, 1, 40), ZT, 64, 64, 2000), ((1, 2, 30), Z2, 96, 64, 2000),
+                                  ((1, 1, 40), Z2, 80, 64, 2000)],
+                         ids=lambda c: f"{c[0]}-{'zt' if c[1] == ZT else 'z2'}-R{c[2]}")
+def test_wl_large_classes(fg, orc, case):
+    """Flip classes longer than one ballot round of walk_wl's sorted arrays (16 entries
+    each way) and longer than a warp (32): naive (2,2,16) has U classes of 16 rows,
+    (2,3,20) of 20, (1,1,40) one U class of all 40 rows.  Every walker, two launches
+    (the second resumes from the class image), with the structure self-check on."""
+    (m, n, p), ring, R, W, steps = case
+    seed = 0x3D + R
+    os.environ["FG_DBG"] = "1"
+    try:
+        g = _ctx(fg, "wl", m, n, p, ring, R, W)
+        g.seed_naive()
+        g.walk(steps, seed, fg.params_default(phase_steps=steps // 2 + 1))
+    finally:
+        del os.environ["FG_DBG"]
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
+    _check(got, ref, None)
