@@ -1,33 +1,29 @@
 // fg_walk_wl.cuh -- the RandomWalk kernel (Algorithm 1) for walkers
 // with 33..512 rows and wide factors (configs C4 and C5: (5,5,5) R = 160 with 25-element
 // factors, (4,5,12) / (5,6,10) / (6,7,9) R = 256 / 320 / 416 with up to 63 elements).
-// ONE WALKER PER WARP with the flip classes kept as SORTED ARRAYS.
+// ONE WALKER PER WARP with LINKED CLASSES, rows round-robin over the lanes.
 //
-// Why: a flip changes one factor of two rows; the class bookkeeping of R10 needs, for the
-// old and the new key of each, the class members below the row (their later counts
-// change) and the members above (the row's own later count).  Round 1's walk_wm and the
-// first walk_wl found them with a compare pass over all r rows (O(r) 128-bit compares per
-// change: 60 % of the C5 instruction stream).  Here every role X keeps its live rows
-// sorted by (key, row index):
-//   sa[X][i]   the i-th row in that order          pos[X][l]  the index of row l in sa[X]
-// so a class is a contiguous run ordered by row, a key's run is found by a 32-ary
-// search (two ballot rounds at r = 416), the members below / above a row are the run
-// entries before / after it, the t-th later member of row i is sa[X][pos[X][i] + t + 1]
-// (the draw needs no pointer chasing), and a key change moves ONE entry (a block shift of
-// the entries between the old and the new position, warp-parallel).  Per row l:
+// Why: walk_wm (fg_walk_multi.cuh) finds the second row of every draw with a compare
+// sweep over all rows and keeps per-row class counts in registers (local memory for
+// NS > 8); walk_ql's quad mapping keeps linked class lists but needs 8 walkers' state
+// per warp, which does not fit shared memory for R >= 160 two-word factors.  Here one
+// walker per warp keeps, per row l (lane l % 32, word l / 32):
 //   fac[X][l]  factor X (U and V sign-normalised; W up to sign)
-//   wsb        the signs of the w factors, one bit per row (the W key is the positive form)
+//   nxh[X][l]  the next row of l's class in role X (1023 = none)
+//   wsb        the signs of the w factors, one bit per row (the stored W key is the
+//              positive form, W classes are "equal up to sign")
 //   lc[l]      later counts of the three classes, 10 bits each (R10)
 //   tw[w]      per 32-row word the sum of its rows' later counts (U | V << 16; W)
-// A draw (R11) is a lookup in the per-step prefix of the word totals, one warp scan of
-// the word's later counts and one sa read.  R12's skip test (does a touched row share two
-// factors with another row?) scans the three runs such a row must lie in.  The sorted
-// arrays, later counts and word totals survive between launches in an HBM image
-// (WalkArgs::wl_img; pos is rebuilt from sa).  Zero keys are in no class (R10).
+// so a draw (R11) is a lookup in the per-step prefix of the word totals, one warp scan
+// of the word's later counts and `hops` next-pointer steps, and a flip commit is ONE
+// compare pass over the rows
+// for both changed factors (they are in different roles, so the two class updates
+// commute) that also gives R12's exact skip test (does a touched row share two
+// factors with another row?), as in walk_ql.  The class structure (nx, lc, tw and the
+// candidate totals) survives between launches in an HBM image (WalkArgs::wl_img).
 //
 // Same readings (R8-R23), draw order and digest as the oracle and the other kernels;
-// parity: tests/test_gpu_parity.py, tests/test_gpu_fullsize.py, tests/test_gpu_fuzz.py,
-// tests/test_gpu_kernels.py (FG_DBG=1 adds a full structure self-check after every step).
+// parity: tests/test_gpu_parity.py, tests/test_gpu_fullsize.py, tests/test_gpu_fuzz.py.
 #pragma once
 #include <cstdlib>
 #include <type_traits>
@@ -36,42 +32,40 @@
 namespace fgwl {
 using namespace fgd;
 
+constexpr int NIL = 1023;
 constexpr int PXS = 9;                         // Philox table stride (32 steps x 9 words)
 constexpr int IMG_SCALARS = 8;                 // nCU, nCV, nCW, dset lo, dset hi, nD, dover, r
 
-// class image per walker (HBM): sa (3 RM u16), lc (RM), tw (32), wsb (16), scalars
+// class image per walker (HBM): nxh (3 RM u16), lc (RM), tw (32), wsb (16), scalars
 __host__ __device__ constexpr int img_words(int nwd) { return 48 * nwd + 32 * nwd + 32 + 16 + IMG_SCALARS; }
 
+__device__ __forceinline__ uint32_t below_in(int l, int w)      // bits of word w for rows < l
+{
+    const int b = l - 32 * w;
+    return b <= 0 ? 0u : (b >= 32 ? 0xFFFFFFFFu : ((1u << b) - 1u));
+}
+__device__ __forceinline__ uint32_t above_in(int l, int w)      // bits of word w for rows > l
+{
+    const int b = l - 32 * w;
+    return b < 0 ? 0xFFFFFFFFu : (b >= 31 ? 0u : ~((2u << b) - 1u));
+}
 __device__ __forceinline__ uint32_t setf(uint32_t x, int X, int v)
 {
     return (x & ~(1023u << (10 * X))) | ((uint32_t)v << (10 * X));
 }
 __device__ __forceinline__ int getf(uint32_t x, int X) { return (int)((x >> (10 * X)) & 1023u); }
 
-// total order on keys (any order consistent with P::eq; zero keys sort first)
-template <class P> __device__ __forceinline__ bool klt(typename P::F a, typename P::F b)
-{
-    if constexpr (std::is_integral<typename P::F>::value) return a < b;
-    else return a.d < b.d || (a.d == b.d && a.s < b.s);
-}
-
 // one walker's shared-memory state
 template <class P> struct WS {
     typename P::F *fac;   // [3][RM]
-    uint16_t *sa;         // [3][RM]
-    uint16_t *pos;        // [3][RM]
+    uint16_t *nxh;        // [3][RM]
     uint32_t *lc;         // [RM]
     uint32_t *wsb;        // [16]
     uint32_t *tw;         // [32]: U | V << 16 at w, W at 16 + w
     int nwd, RM;
     __device__ __forceinline__ typename P::F key(int X, int l) const { return fac[X * RM + l]; }
-    __device__ __forceinline__ int at(int X, int i) const { return (int)sa[X * RM + i]; }
-    __device__ __forceinline__ int where(int X, int l) const { return (int)pos[X * RM + l]; }
-    __device__ __forceinline__ void put(int X, int i, int l) const
-    {
-        sa[X * RM + i] = (uint16_t)l;
-        pos[X * RM + l] = (uint16_t)i;
-    }
+    __device__ __forceinline__ int nxt(int X, int l) const { return (int)nxh[X * RM + l]; }
+    __device__ __forceinline__ void set_nxt(int X, int l, int v) const { nxh[X * RM + l] = (uint16_t)v; }
     __device__ __forceinline__ uint32_t wsg(int l) const { return (wsb[l >> 5] >> (l & 31)) & 1u; }
     __device__ __forceinline__ void set_wsg(int l, uint32_t v) const      // lane 0
     {
@@ -90,226 +84,82 @@ template <class P> struct WS {
         o.w = full(2, l);
         return o;
     }
-    // word total of role X += d (any lane; shared-memory atomic: several lanes may hit
-    // one word; the packed U | V << 16 fields never borrow since totals stay >= 0)
+    // word total of role X (lane 0 only)
     __device__ __forceinline__ void tw_add(int w, int X, int d) const
     {
-        if (X == 2) atomicAdd(tw + 16 + w, (uint32_t)d);
-        else atomicAdd(tw + w, (uint32_t)d << (16 * X));
+        if (X == 2) tw[16 + w] += (uint32_t)d;
+        else tw[w] += (uint32_t)d << (16 * X);
     }
 };
 
-// ---- sorted-array primitives (whole warp; callers keep the warp converged) ----
-
-// first index i in [0, r) with (key(sa[i]), sa[i]) >= (k, t), else r: 32-ary search
+// Row t's role-X key goes from o to k (a zero key is in no class, R10: zero factors
+// never pair): one compare pass over the live rows (< r), then the class list, the
+// later counts and the word totals are relinked.  Returns the change of the role's
+// candidate-pair count.  Whole warp; rare paths only (the flip commit has its own
+// fused two-change pass in the kernel).
 template <class P>
-__device__ __forceinline__ int lower_bound(const WS<P> &s, int r, int X, typename P::F k, int t)
+__device__ __noinline__ int key_change(WS<P> s, int r, int t, int X, typename P::F o, typename P::F k)
 {
+    typedef typename P::F F;
     const int lane = threadIdx.x & 31;
-    int lo = 0, hi = r;
+    const bool zo = P::zero(o), zk = P::zero(k);
+    int pO = NIL, sO = NIL, pK = NIL, sK = NIL, aK = 0, tO = 0, tK = 0;
+    const F *fx = s.fac + X * s.RM;
 #pragma unroll 1
-    while (hi > lo) {
-        const int step = (hi - lo + 31) >> 5;
-        const int p = lo + lane * step;
-        bool less = false;
-        if (p < hi) {
-            const int m = s.at(X, p);
-            const typename P::F km = s.key(X, m);
-            less = klt<P>(km, k) || (P::eq(km, k) && m < t);
-        }
-        const int c = __popc(__ballot_sync(FULL, less));
-        if (c == 0) break;
-        const int nlo = lo + (c - 1) * step + 1;
-        const int nhi = lo + c * step;
-        lo = nlo;
-        hi = nhi < hi ? nhi : hi;
-    }
-    return lo;
-}
-
-// number of consecutive entries with key k ending at index i-1 (i-1, i-2, ...), rows > rmin
-template <class P>
-__device__ __forceinline__ int run_back(const WS<P> &s, int X, int i, typename P::F k, int rmin)
-{
-    const int lane = threadIdx.x & 31;
-    int n = 0;
-#pragma unroll 1
-    for (;;) {
-        const int idx = i - 1 - n - lane;
-        bool e = false;
-        if (idx >= 0) {
-            const int m = s.at(X, idx);
-            e = m > rmin && P::eq(s.key(X, m), k);
-        }
-        const uint32_t b = __ballot_sync(FULL, e);
-        const int c = b == FULL ? 32 : __ffs(~b) - 1;
-        n += c;
-        if (c < 32) return n;
-    }
-}
-// number of consecutive entries with key k starting at index i (i, i+1, ... < r)
-template <class P>
-__device__ __forceinline__ int run_fwd(const WS<P> &s, int X, int i, int r, typename P::F k)
-{
-    const int lane = threadIdx.x & 31;
-    int n = 0;
-#pragma unroll 1
-    for (;;) {
-        const int idx = i + n + lane;
-        const bool e = idx < r && P::eq(s.key(X, s.at(X, idx)), k);
-        const uint32_t b = __ballot_sync(FULL, e);
-        const int c = b == FULL ? 32 : __ffs(~b) - 1;
-        n += c;
-        if (c < 32) return n;
-    }
-}
-// the run of key k around index p (the entry at p excluded): nb entries before, na after.
-// One ballot round covers 16 entries each way (flip classes are small); longer runs
-// continue with run_back / run_fwd.
-template <class P>
-__device__ __forceinline__ void run_both(const WS<P> &s, int X, int p, int r, typename P::F k, int &nb, int &na)
-{
-    const int lane = threadIdx.x & 31;
-    const int idx = lane < 16 ? p - 1 - lane : p + 1 + (lane - 16);
-    const bool e = idx >= 0 && idx < r && P::eq(s.key(X, s.at(X, idx)), k);
-    const uint32_t b = __ballot_sync(FULL, e);
-    const uint32_t lo = b & 0xFFFFu, hi = b >> 16;          // ffs(~x) - 1 <= 16
-    nb = __ffs(~lo) - 1;
-    na = __ffs(~hi) - 1;
-    if (nb == 16) nb += run_back(s, X, p - 16, k, -1);
-    if (na == 16) na += run_fwd(s, X, p + 17, r, k);
-}
-// the rows at sa[X][i0 .. i0+n) gain (d = +1) or lose (d = -1) one later member in role X
-template <class P>
-__device__ __forceinline__ void members_add(const WS<P> &s, int X, int i0, int n, int d)
-{
-    const int lane = threadIdx.x & 31;
-#pragma unroll 1
-    for (int k = lane; k < n; k += 32) {
-        const int m = s.at(X, i0 + k);
-        s.lc[m] += d > 0 ? (1u << (10 * X)) : (0u - (1u << (10 * X)));
-        s.tw_add(m >> 5, X, d);
-    }
-}
-// move the entry at index `from` to index `to` (the entries between shift by one) and
-// make it row t (a rename when t differs from the moved row)
-template <class P>
-__device__ __forceinline__ void move_entry(const WS<P> &s, int X, int from, int to, int t)
-{
-    const int lane = threadIdx.x & 31;
-    if (to > from) {
-#pragma unroll 1
-        for (int b = from; b < to; b += 32) {
-            const int i = b + lane;
-            const int v = i < to ? s.at(X, i + 1) : 0;
-            __syncwarp();
-            if (i < to) s.put(X, i, v);
-        }
-    } else if (to < from) {
-#pragma unroll 1
-        for (int b = from; b > to; b -= 32) {
-            const int i = b - lane;
-            const int v = i > to ? s.at(X, i - 1) : 0;
-            __syncwarp();
-            if (i > to) s.put(X, i, v);
-        }
+    for (int w = 0; w < s.nwd; ++w) {
+        const int l = 32 * w + lane;
+        const F x = fx[l];
+        const bool live = l < r && l != t;
+        const bool eo = live && !zo && P::eq(x, o);
+        const bool ek = live && !zk && P::eq(x, k);
+        const uint32_t mO = __ballot_sync(FULL, eo), mK = __ballot_sync(FULL, ek);
+        if ((mO | mK) == 0u) continue;
+        if (l < t && eo != ek) s.lc[l] += ek ? (1u << (10 * X)) : (0u - (1u << (10 * X)));
+        const uint32_t bl = below_in(t, w), ab = above_in(t, w);
+        if (mO & bl) pO = 32 * w + 31 - __clz(mO & bl);
+        if ((mO & ab) && sO == NIL) sO = 32 * w + __ffs(mO & ab) - 1;
+        if (mK & bl) pK = 32 * w + 31 - __clz(mK & bl);
+        if ((mK & ab) && sK == NIL) sK = 32 * w + __ffs(mK & ab) - 1;
+        aK += __popc(mK & ab);
+        tO += __popc(mO);
+        tK += __popc(mK);
+        const int d = __popc(mK & bl) - __popc(mO & bl);
+        if (lane == 0 && d) s.tw_add(w, X, d);
     }
     __syncwarp();
-    if (lane == 0) s.put(X, to, t);
-    __syncwarp();
-}
-
-// Row t's role-X key goes from o to k (t live, in sa[X]).  Returns the change of the
-// role's candidate-pair count.  Whole warp.  (Inlined once on the flip path; rare paths
-// call the out-of-line copy.)
-template <class P>
-__device__ __forceinline__ int change_key_inl(const WS<P> &s, int r, int t, int X, typename P::F o, typename P::F k)
-{
-    const int lane = threadIdx.x & 31;
-    const int p = s.where(X, t);
-    int d = 0, na = 0;
-    if (!P::zero(o)) {
-        int nb;
-        run_both(s, X, p, r, o, nb, na);                 // members below / above t
-        members_add(s, X, p - nb, nb, -1);
-        d -= nb + na;
-    }
-    // t's entry still holds key o (outside k's run): the position among the others
-    const int ins = lower_bound(s, r, X, k, t);
-    int nak = 0;
-    if (!P::zero(k)) {
-        // entries ins-1, ins-2, ... and ins, ins+1, ...: run_both around the virtual slot
-        // between ins-1 and ins (index ins-1 as the excluded centre would drop ins-1; use
-        // the two one-sided counts)
-        const int nbk = run_back(s, X, ins, k, -1);
-        nak = run_fwd(s, X, ins, r, k);
-        members_add(s, X, ins - nbk, nbk, +1);
-        d += nbk + nak;
-    }
-    __syncwarp();
-    move_entry(s, X, p, ins > p ? ins - 1 : ins, t);
     if (lane == 0) {
+        if (pO != NIL) s.set_nxt(X, pO, sO);
+        if (pK != NIL) s.set_nxt(X, pK, t);
+        s.set_nxt(X, t, sK);
+        const int old = getf(s.lc[t], X);
+        s.lc[t] = setf(s.lc[t], X, aK);
+        s.tw_add(t >> 5, X, aK - old);
         s.fac[X * s.RM + t] = k;
-        s.lc[t] = setf(s.lc[t], X, nak);
-        if (nak != na) s.tw_add(t >> 5, X, nak - na);
     }
     __syncwarp();
-    return d;
-}
-template <class P>
-__device__ __noinline__ int change_key(WS<P> s, int r, int t, int X, typename P::F o, typename P::F k)
-{
-    return change_key_inl<P>(s, r, t, X, o, k);
-}
-
-// a new row t (not yet in sa[X], r entries there) with role-X key k.  Whole warp.
-template <class P>
-__device__ __noinline__ int insert_key(WS<P> s, int r, int t, int X, typename P::F k)
-{
-    const int lane = threadIdx.x & 31;
-    const int ins = lower_bound(s, r, X, k, t);
-    int d = 0, nak = 0;
-    if (!P::zero(k)) {
-        const int nbk = run_back(s, X, ins, k, -1);
-        nak = run_fwd(s, X, ins, r, k);
-        members_add(s, X, ins - nbk, nbk, +1);
-        d = nbk + nak;
-    }
-    __syncwarp();
-    move_entry(s, X, r, ins, t);          // entries [ins, r) shift up by one
-    if (lane == 0) {
-        s.fac[X * s.RM + t] = k;
-        s.lc[t] = setf(s.lc[t], X, nak);
-        if (nak) s.tw_add(t >> 5, X, nak);
-    }
-    __syncwarp();
-    return d;
+    return tK - tO;
 }
 
 struct D3 { int d0, d1, d2; };
 
 // Row l becomes nr (a normalised row): a class update for every role whose key changes
-// (all three if `fresh`: l is a new row, r entries in the arrays), and the W sign bit.
+// (all three if `fresh`: l is a new row, in no class yet), and the W sign bit.
 template <class P>
 __device__ __noinline__ D3 set_row(WS<P> s, int r, int l, Row<P> nr, bool fresh)
 {
     const int lane = threadIdx.x & 31;
     D3 d = {0, 0, 0};
     if (fresh) {
-        if (lane == 0) s.lc[l] = 0u;
+        if (lane == 0) { s.set_nxt(0, l, NIL); s.set_nxt(1, l, NIL); s.set_nxt(2, l, NIL); s.lc[l] = 0u; }
         __syncwarp();
     }
 #pragma unroll 1
     for (int X = 0; X < 3; ++X) {
         const typename P::F k = X == 0 ? nr.u : (X == 1 ? nr.v : P::abs(nr.w));
-        int v = 0;
-        if (fresh) {
-            v = insert_key<P>(s, r, l, X, k);
-        } else {
-            const typename P::F o = s.key(X, l);
-            if (P::eq(o, k)) continue;
-            v = change_key<P>(s, r, l, X, o, k);
-        }
+        typename P::F o = s.key(X, l);
+        if (fresh) o = P::make(0, 0);
+        if (!fresh && P::eq(o, k)) continue;
+        const int v = key_change<P>(s, r, l, X, o, k);
         d.d0 += X == 0 ? v : 0;
         d.d1 += X == 1 ? v : 0;
         d.d2 += X == 2 ? v : 0;
@@ -322,9 +172,9 @@ __device__ __noinline__ D3 set_row(WS<P> s, int r, int l, Row<P> nr, bool fresh)
 template <class P> struct Found { int j; Row<P> mg; };
 
 // The first row l >= lmin, l != t (ascending) with reducible(row t, row l) (R13), and
-// the merged row (row t as base); j = -1 if none.  A row sharing two factor keys with
-// row t (W up to sign) is in t's U class or its V class: candidates come from those two
-// runs, ascending, each checked exactly.  Whole warp.
+// the merged row (row t as base); j = -1 if none.  Candidates share two factor keys
+// with row t (W up to sign, zero keys included: the oracle compares zero factors as
+// equal); each is checked exactly.  Whole warp.
 template <class P>
 __device__ __noinline__ Found<P> first_reducible(WS<P> s, int r, int t, int lmin)
 {
@@ -335,38 +185,23 @@ __device__ __noinline__ Found<P> first_reducible(WS<P> s, int r, int t, int lmin
     Found<P> out;
     out.j = -1;
     out.mg = rt;
-    // the two runs: [a0, a0 + n0) in sa[U], [a1, a1 + n1) in sa[V] (t itself included)
-    const int p0 = s.where(0, t), p1 = s.where(1, t);
-    const int b0 = run_back(s, 0, p0, k0, -1), b1 = run_back(s, 1, p1, k1, -1);
-    const int a0 = p0 - b0, a1 = p1 - b1;
-    const int n0 = b0 + 1 + run_fwd(s, 0, p0 + 1, r, k0);
-    const int n1 = b1 + 1 + run_fwd(s, 1, p1 + 1, r, k1);
-    int cur = lmin - 1;
 #pragma unroll 1
-    for (;;) {
-        // smallest candidate row > cur over both runs (chunks of 32 per run)
-        int best = 0x7fffffff;
-#pragma unroll 1
-        for (int c = lane; c < n0; c += 32) {
-            const int m = s.at(0, a0 + c);
-            if (m > cur && m != t && m < best && (P::eq(s.key(1, m), k1) || P::eq(s.key(2, m), k2))) best = m;
+    for (int w = 0; w < s.nwd; ++w) {
+        const int l = 32 * w + lane;
+        const int c = (int)P::eq(s.key(0, l), k0) + (int)P::eq(s.key(1, l), k1) + (int)P::eq(s.key(2, l), k2);
+        uint32_t m = __ballot_sync(FULL, l < r && l != t && l >= lmin && c >= 2);
+        while (m) {
+            const int j = 32 * w + __ffs(m) - 1;
+            m &= m - 1u;
+            Row<P> mg;
+            if (reducible<P>(rt, s.row(j), mg)) {
+                out.j = j;
+                out.mg = mg;
+                return out;
+            }
         }
-#pragma unroll 1
-        for (int c = lane; c < n1; c += 32) {
-            const int m = s.at(1, a1 + c);
-            // rows sharing U as well are U-run candidates already
-            if (m > cur && m != t && m < best && P::eq(s.key(2, m), k2)) best = m;
-        }
-        best = (int)__reduce_min_sync(FULL, (uint32_t)best);
-        if (best == 0x7fffffff) return out;
-        Row<P> mg;
-        if (reducible<P>(rt, s.row(best), mg)) {
-            out.j = best;
-            out.mg = mg;
-            return out;
-        }
-        cur = best;
     }
+    return out;
 }
 
 // Debug only (FG_DBG bit 0): rebuild the class structure from the rows and compare.
@@ -378,24 +213,16 @@ __device__ __noinline__ uint32_t check_structure(WS<P> s, int r, uint32_t nCU, u
     uint32_t bad = 0;
     uint32_t tot[3] = {0, 0, 0};
     for (int X = 0; X < 3; ++X) {
-        for (int i = lane; i < r; i += 32) {
-            const int m = s.at(X, i);
-            if (m >= r || s.where(X, m) != i) bad |= 16u;
-            if (i + 1 < r) {
-                const int n = s.at(X, i + 1);
-                const typename P::F km = s.key(X, m), kn = s.key(X, n);
-                if (!(klt<P>(km, kn) || (P::eq(km, kn) && m < n))) bad |= 32u;
-            }
-        }
         for (int w = 0; w < s.nwd; ++w) {
             const int l = 32 * w + lane;
-            int cnt = 0;
+            int cnt = 0, first = NIL;
             if (l < r) {
                 const typename P::F k = s.key(X, l);
                 if (!P::zero(k))
                     for (int j = l + 1; j < r; ++j)
-                        if (P::eq(s.key(X, j), k)) cnt++;
+                        if (P::eq(s.key(X, j), k)) { if (first == NIL) first = j; cnt++; }
                 if (getf(s.lc[l], X) != cnt) bad |= 1u;
+                if (s.nxt(X, l) != first) bad |= 2u;
             }
             const int sum = __reduce_add_sync(FULL, (uint32_t)cnt);
             const uint32_t t = X == 2 ? s.tw[16 + w] : ((s.tw[w] >> (16 * X)) & 0xFFFFu);
@@ -420,8 +247,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
     s.wsb = s.tw + 32;
     uint32_t *px = s.wsb + 16;                                 // Philox table [32][PXS]
     uint32_t *rc = px + 32 * PXS;                              // 8 rare counters
-    s.sa = reinterpret_cast<uint16_t *>(rc + 8);
-    s.pos = s.sa + 3 * RM;
+    s.nxh = reinterpret_cast<uint16_t *>(rc + 8);
     s.nwd = nwd;
     s.RM = RM;
     const int lane = threadIdx.x;
@@ -459,6 +285,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             s.fac[l] = u;
             s.fac[RM + l] = v;
             s.fac[2 * RM + l] = P::abs(w);
+            s.set_nxt(0, l, NIL); s.set_nxt(1, l, NIL); s.set_nxt(2, l, NIL);
             s.lc[l] = 0u;
             const uint32_t sg = __ballot_sync(FULL, P::first_neg(w));
             if (lane == 0) s.wsb[l >> 5] = sg;
@@ -475,9 +302,9 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
         uint32_t *img = a.wl_img ? a.wl_img + (size_t)wk * IMGW : nullptr;
         const bool resume = img != nullptr && a.img_valid && (int)img[IMGW - 1] == r;
         if (resume) {
-            const uint32_t *sai = img, *lci = img + 3 * RM / 2, *twi = lci + RM;
+            const uint32_t *nxi = img, *lci = img + 3 * RM / 2, *twi = lci + RM;
 #pragma unroll 1
-            for (int k = lane; k < 3 * RM / 2; k += 32) reinterpret_cast<uint32_t *>(s.sa)[k] = sai[k];
+            for (int k = lane; k < 3 * RM / 2; k += 32) reinterpret_cast<uint32_t *>(s.nxh)[k] = nxi[k];
 #pragma unroll 1
             for (int l = lane; l < RM; l += 32) s.lc[l] = lci[l];
             s.tw[lane] = twi[lane];
@@ -487,51 +314,30 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             dset = (uint64_t)sc[3] | ((uint64_t)sc[4] << 32);
             nD = (int)sc[5];
             dover = sc[6] != 0u;
-            __syncwarp();
-#pragma unroll 1
-            for (int X = 0; X < 3; ++X)
-#pragma unroll 1
-                for (int i = lane; i < r; i += 32) s.pos[X * RM + s.at(X, i)] = (uint16_t)i;
         } else {
-            // sorted arrays by rank (O(r^2 / 32) per lane, once per walker), then the later
-            // counts from the runs
+            // class links and later counts from the rows: O(r^2 / 32) per lane
 #pragma unroll 1
             for (int X = 0; X < 3; ++X) {
 #pragma unroll 1
-                for (int l = lane; l < r; l += 32) {
-                    const F k = s.key(X, l);
-                    int rank = 0;
-#pragma unroll 1
-                    for (int m = 0; m < r; ++m) {
-                        const F km = s.key(X, m);
-                        rank += (klt<P>(km, k) || (P::eq(km, k) && m < l)) ? 1 : 0;
-                    }
-                    s.put(X, rank, l);
-                }
-                __syncwarp();
-#pragma unroll 1
                 for (int w = 0; w < nwd; ++w) {
                     const int l = 32 * w + lane;
-                    int cnt = 0;
+                    int cnt = 0, first = NIL;
                     if (l < r) {
                         const F k = s.key(X, l);
                         if (!P::zero(k)) {
-                            const int p = s.where(X, l);
 #pragma unroll 1
-                            for (int i = p + 1; i < r && P::eq(s.key(X, s.at(X, i)), k); ++i) cnt++;
+                            for (int j = l + 1; j < r; ++j)
+                                if (P::eq(s.key(X, j), k)) { if (first == NIL) first = j; cnt++; }
                         }
                     }
+                    s.set_nxt(X, l, first);
                     s.lc[l] = setf(s.lc[l], X, cnt);
                     const uint32_t sum = __reduce_add_sync(FULL, (uint32_t)cnt);
-                    if (lane == 0) {
-                        if (X == 2) s.tw[16 + w] += sum;
-                        else s.tw[w] += sum << (16 * X);
-                    }
+                    if (lane == 0) s.tw_add(w, X, (int)sum);
                     nCU += X == 0 ? sum : 0u;
                     nCV += X == 1 ? sum : 0u;
                     nCW += X == 2 ? sum : 0u;
                 }
-                __syncwarp();
             }
         }
         __syncwarp();
@@ -552,63 +358,25 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             dset |= (uint64_t)x << (10 * nD);
             nD++;
         };
-        // R14 remove(h) with the 2-entry worklist (entries == h dropped, r-1 -> h): h's
-        // entries leave the arrays; row r-1's entries are renamed h and move down past
-        // the members of its classes that lie in (h, r-1)
+        // R14 remove(h) with the 2-entry worklist (entries == h dropped, r-1 -> h): h
+        // leaves its classes; row r-1 leaves its classes and re-enters them as row h
         auto remove_row = [&](int h, int &wl0, int &wl1, int &nwl) {
             const int last = r - 1;
+            const Row<P> lastrow = s.row(last);
 #pragma unroll 1
-            for (int X = 0; X < 3; ++X) {
-                const F o = s.key(X, h);
-                const int p = s.where(X, h);
-                int na = 0;
-                if (!P::zero(o)) {
-                    const int nb = run_back(s, X, p, o, -1);
-                    na = run_fwd(s, X, p + 1, r, o);
-                    members_add(s, X, p - nb, nb, -1);
-                    const int v = -(nb + na);
+            for (int k = 0; k < 2; ++k) {
+                const int t = k == 0 ? h : last;
+                if (k == 1 && h == last) break;
+#pragma unroll 1
+                for (int X = 0; X < 3; ++X) {
+                    const int v = key_change<P>(s, r, t, X, s.key(X, t), P::make(0, 0));
                     nCU += X == 0 ? (uint32_t)v : 0u;
                     nCV += X == 1 ? (uint32_t)v : 0u;
                     nCW += X == 2 ? (uint32_t)v : 0u;
                 }
-                __syncwarp();
-                move_entry(s, X, p, r - 1, h);     // h's entry to the end (dropped below)
-                if (lane == 0 && na) s.tw_add(h >> 5, X, -na);
-                __syncwarp();
-            }
-            // the arrays now hold r-1 live entries [0, r-1); h's lc contributions are gone
-            if (lane == 0) s.lc[h] = 0u;
-            __syncwarp();
-            if (h != last) {
-                uint32_t lch = 0;
-#pragma unroll 1
-                for (int X = 0; X < 3; ++X) {
-                    const F kl = s.key(X, last);
-                    const int p = s.where(X, last);
-                    int c = 0;
-                    if (!P::zero(kl)) {
-                        c = run_back(s, X, p, kl, h);          // members in (h, last)
-                        members_add(s, X, p - c, c, -1);
-                    }
-                    __syncwarp();
-                    move_entry(s, X, p, p - c, h);
-                    lch |= (uint32_t)c << (10 * X);
-                    if (lane == 0 && c) s.tw_add(h >> 5, X, c);
-                    __syncwarp();
-                }
-                const Row<P> lastrow = s.row(last);
-                __syncwarp();
-                if (lane == 0) {
-                    s.fac[h] = s.fac[last];
-                    s.fac[RM + h] = s.fac[RM + last];
-                    s.fac[2 * RM + h] = s.fac[2 * RM + last];
-                    s.lc[h] = lch;
-                    s.lc[last] = 0u;
-                    s.set_wsg(h, P::first_neg(lastrow.w) ? 1u : 0u);
-                }
-                __syncwarp();
             }
             r--;
+            if (h != last) addC(set_row<P>(s, r, h, lastrow, true));
             int n2 = 0, x0 = 0, x1 = 0;
             if (nwl >= 1 && wl0 != h) { x0 = wl0; n2 = 1; }
             if (nwl >= 2 && wl1 != h) { if (n2 == 0) x0 = wl1; else x1 = wl1; n2++; }
@@ -777,6 +545,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
         };
 
         // copy of the current rows to an HBM scheme image (best / verify queue): rows < n
+        // (n >= r; zeros for r <= t < n)
         auto store_rows = [&](uint64_t *dst, int n) {
 #pragma unroll 1
             for (int t = lane; t < n; t += 32) {
@@ -795,27 +564,6 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
 #pragma unroll 1
             for (int l = lane; l < r; l += 32) v += P::popd(s.key(0, l)) + P::popd(s.key(1, l)) + P::popd(s.key(2, l));
             return (int)__reduce_add_sync(FULL, (uint32_t)v);
-        };
-        // does a row other than a0, b0 in the run of sa[X] around index p share two factor
-        // keys with row a0 or with row b0?  (keys as stored: W up to sign)
-        auto run_two = [&](int X, int p, int a0, int b0) -> bool {
-            const F k = s.key(X, s.at(X, p));
-            int nb, na;
-            run_both(s, X, p, r, k, nb, na);
-            const int n = nb + 1 + na;
-            const F x0 = s.key(0, a0), y0 = s.key(1, a0), z0 = s.key(2, a0);
-            const F x1 = s.key(0, b0), y1 = s.key(1, b0), z1 = s.key(2, b0);
-            bool h = false;
-#pragma unroll 1
-            for (int c = lane; c < n; c += 32) {
-                const int m = s.at(X, p - nb + c);
-                if (m == a0 || m == b0) continue;
-                const F mx = s.key(0, m), my = s.key(1, m), mz = s.key(2, m);
-                const int c0 = (int)P::eq(mx, x0) + (int)P::eq(my, y0) + (int)P::eq(mz, z0);
-                const int c1 = (int)P::eq(mx, x1) + (int)P::eq(my, y1) + (int)P::eq(mz, z1);
-                h = h || c0 >= 2 || c1 >= 2;
-            }
-            return __any_sync(FULL, h);
         };
 
         int boff = 32;
@@ -895,9 +643,11 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     }
                     const int L = __ffs(__ballot_sync(FULL, inc2 > q1)) - 1;
                     const int i = 32 * wsel + L;
-                    // j: the (q1 - acc)-th later member of row i's X class = the entry
-                    // (q1 - acc + 1) places after row i in sa[X]
-                    const int j = s.at(X, s.where(X, i) + (int)(q1 - __shfl_sync(FULL, inc2 - lv, L)) + 1);
+                    // j: the (q1 - acc)-th later member of row i's X class
+                    const uint16_t *nxX = s.nxh + X * RM;
+                    int j = i;
+#pragma unroll 1
+                    for (uint32_t hops = q1 - __shfl_sync(FULL, inc2 - lv, L) + 1; hops; --hops) j = nxX[j];
                     const int al = d ? j : i, be = d ? i : j;
                     // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e
                     const unsigned yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
@@ -934,39 +684,89 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                 const bool fa = P::first_neg(fny), fb = P::first_neg(fnz);
                 const F kY = fY == 2 ? P::abs(fny) : P::sel(fa, P::neg(fny), fny);
                 const F kZ = fZ == 2 ? P::abs(fnz) : P::sel(fb, P::neg(fnz), fnz);
-                const uint32_t sa_ = fY == 2 ? (uint32_t)fa : (s.wsg(alpha) ^ (uint32_t)fa);
-                const uint32_t sb_ = fZ == 2 ? (uint32_t)fb : (s.wsg(beta) ^ (uint32_t)fb);
+                const uint32_t sa = fY == 2 ? (uint32_t)fa : (s.wsg(alpha) ^ (uint32_t)fa);
+                const uint32_t sb = fZ == 2 ? (uint32_t)fb : (s.wsg(beta) ^ (uint32_t)fb);
                 const F oY = s.key(fY, alpha), oZ = s.key(fZ, beta);
-                // R12: alpha after the commit = (AX, kY, AZ), beta = (AX, BY, kZ) (alpha and
-                // beta share the X key: they are in one X class); the pair itself shares X
-                // plus Y (kY vs BY) or Z (AZ vs kZ)
+                // R12 test keys: alpha after the commit = (AX, kY, AZ), beta = (AX, BY, kZ)
+                // (alpha and beta share the X key: they are in one X class)
+                const F AX = s.key(fX, alpha), AZ = s.key(fZ, alpha), BY = s.key(fY, beta);
                 const bool zY = P::zero(kY), zZ = P::zero(kZ);
-                const bool pair2 = P::eq(kY, s.key(fY, beta)) || P::eq(s.key(fZ, alpha), kZ);
-                // class updates of (alpha, Y) and (beta, Z): different roles, independent
-                int dY = 0, dZ = 0;
-#pragma unroll 1
-                for (int c = 0; c < 2; ++c) {
-                    const F o = c ? oZ : oY, k = c ? kZ : kY;
-                    if (P::eq(o, k)) continue;
-                    const int v = change_key_inl<P>(s, r, c ? beta : alpha, c ? fZ : fY, o, k);
-                    dY += c ? 0 : v;
-                    dZ += c ? v : 0;
+                const F *pX = s.fac + fX * RM, *pY = s.fac + fY * RM, *pZ = s.fac + fZ * RM;
+                // fused compare pass: class updates of (alpha, Y) and (beta, Z) + R12 test
+                int pO0 = NIL, sO0 = NIL, pK0 = NIL, sK0 = NIL, aK0 = 0, tD0 = 0;
+                int pO1 = NIL, sO1 = NIL, pK1 = NIL, sK1 = NIL, aK1 = 0, tD1 = 0;
+                bool hit = false;
+                // two words per iteration for the 16-byte layouts (ILP at ~2 resident warps
+                // per scheduler: +2 % on C5); one for P32 (-2 % on C4, scripts/gpu_r02_ab.sh)
+                constexpr int PASS_UNROLL = sizeof(F) > 8 ? 2 : 1;
+#pragma unroll PASS_UNROLL
+                for (int w = 0; w < nwd; ++w) {
+                    const int l = 32 * w + lane;
+                    const F xX = pX[l], xY = pY[l], xZ = pZ[l];
+                    const bool la = l < r && l != alpha, lb = l < r && l != beta;
+                    const bool yO = P::eq(xY, oY), yK = P::eq(xY, kY), yB = P::eq(xY, BY);
+                    const bool zO = P::eq(xZ, oZ), zK = P::eq(xZ, kZ), zA = P::eq(xZ, AZ);
+                    const bool xA = P::eq(xX, AX);
+                    // two shared factors with alpha (yK, zA, xA) or with beta (yB, zK, xA)
+                    const bool two = (yK && (zA || xA)) || (zA && xA) || (yB && (zK || xA)) || (zK && xA);
+                    hit = hit || (la && lb && two);
+                    const uint32_t mO0 = __ballot_sync(FULL, la && yO), mK0 = __ballot_sync(FULL, la && yK);
+                    const uint32_t mO1 = __ballot_sync(FULL, lb && zO), mK1 = __ballot_sync(FULL, lb && zK);
+                    if ((mO0 | mK0 | mO1 | mK1) == 0u) continue;
+                    uint32_t dl = 0;
+                    if (l < alpha && la && yO != yK) dl += yK ? (1u << (10 * fY)) : (0u - (1u << (10 * fY)));
+                    if (l < beta && lb && zO != zK) dl += zK ? (1u << (10 * fZ)) : (0u - (1u << (10 * fZ)));
+                    if (dl) s.lc[l] += dl;
+                    {
+                        const uint32_t bl = below_in(alpha, w), ab = above_in(alpha, w);
+                        if (mO0 & bl) pO0 = 32 * w + 31 - __clz(mO0 & bl);
+                        if ((mO0 & ab) && sO0 == NIL) sO0 = 32 * w + __ffs(mO0 & ab) - 1;
+                        if (mK0 & bl) pK0 = 32 * w + 31 - __clz(mK0 & bl);
+                        if ((mK0 & ab) && sK0 == NIL) sK0 = 32 * w + __ffs(mK0 & ab) - 1;
+                        aK0 += __popc(mK0 & ab);
+                        tD0 += __popc(mK0) - __popc(mO0);
+                        const int dw = __popc(mK0 & bl) - __popc(mO0 & bl);
+                        if (lane == 0 && dw) s.tw_add(w, fY, dw);
+                    }
+                    {
+                        const uint32_t bl = below_in(beta, w), ab = above_in(beta, w);
+                        if (mO1 & bl) pO1 = 32 * w + 31 - __clz(mO1 & bl);
+                        if ((mO1 & ab) && sO1 == NIL) sO1 = 32 * w + __ffs(mO1 & ab) - 1;
+                        if (mK1 & bl) pK1 = 32 * w + 31 - __clz(mK1 & bl);
+                        if ((mK1 & ab) && sK1 == NIL) sK1 = 32 * w + __ffs(mK1 & ab) - 1;
+                        aK1 += __popc(mK1 & ab);
+                        tD1 += __popc(mK1) - __popc(mO1);
+                        const int dw = __popc(mK1 & bl) - __popc(mO1 & bl);
+                        if (lane == 0 && dw) s.tw_add(w, fZ, dw);
+                    }
                 }
+                hit = __any_sync(FULL, hit);
+                __syncwarp();
                 if (lane == 0) {
-                    s.set_wsg(alpha, sa_);
-                    s.set_wsg(beta, sb_);
+                    // (alpha, Y) and (beta, Z): different roles, disjoint fields
+                    if (pO0 != NIL) s.set_nxt(fY, pO0, sO0);
+                    if (pK0 != NIL) s.set_nxt(fY, pK0, alpha);
+                    s.set_nxt(fY, alpha, sK0);
+                    const int old0 = getf(s.lc[alpha], fY);
+                    s.lc[alpha] = setf(s.lc[alpha], fY, aK0);
+                    s.tw_add(alpha >> 5, fY, aK0 - old0);
+                    s.fac[fY * RM + alpha] = kY;
+                    if (pO1 != NIL) s.set_nxt(fZ, pO1, sO1);
+                    if (pK1 != NIL) s.set_nxt(fZ, pK1, beta);
+                    s.set_nxt(fZ, beta, sK1);
+                    const int old1 = getf(s.lc[beta], fZ);
+                    s.lc[beta] = setf(s.lc[beta], fZ, aK1);
+                    s.tw_add(beta >> 5, fZ, aK1 - old1);
+                    s.fac[fZ * RM + beta] = kZ;
+                    s.set_wsg(alpha, sa);
+                    s.set_wsg(beta, sb);
                 }
                 __syncwarp();
-                nCU += (fY == 0 ? (uint32_t)dY : 0u) + (fZ == 0 ? (uint32_t)dZ : 0u);
-                nCV += (fY == 1 ? (uint32_t)dY : 0u) + (fZ == 1 ? (uint32_t)dZ : 0u);
-                nCW += (fY == 2 ? (uint32_t)dY : 0u) + (fZ == 2 ? (uint32_t)dZ : 0u);
-                need_local = zY || zZ || pair2;
-                // skip test: a row sharing two factors with alpha lies in alpha's X or Z
-                // class; with beta in beta's X or Y class
-                if (!need_local)
-                    need_local = run_two(fX, s.where(fX, alpha), alpha, beta) ||
-                                 run_two(fZ, s.where(fZ, alpha), alpha, beta) ||
-                                 run_two(fY, s.where(fY, beta), alpha, beta);
+                nCU += (fY == 0 ? (uint32_t)tD0 : 0u) + (fZ == 0 ? (uint32_t)tD1 : 0u);
+                nCV += (fY == 1 ? (uint32_t)tD0 : 0u) + (fZ == 1 ? (uint32_t)tD1 : 0u);
+                nCW += (fY == 2 ? (uint32_t)tD0 : 0u) + (fZ == 2 ? (uint32_t)tD1 : 0u);
+                // the pair itself: X shared, plus Y (kY vs BY) or Z (AZ vs kZ)
+                need_local = zY || zZ || hit || P::eq(kY, BY) || P::eq(AZ, kZ);
             }
 
             uint32_t exp_flag = 0;
@@ -993,7 +793,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                         if (lane == 0) slot = atomicAdd(a.q_count, 1u);
                         slot = __shfl_sync(FULL, slot, 0);
                         if (slot < a.q_cap) {
-                            store_rows(a.q_planes + (size_t)slot * FG_PLANES * R, r);
+                            store_rows(a.q_planes + (size_t)slot * FG_PLANES * R, r);   // verifier reads rank rows
                             if (lane == 0) {
                                 fg_qmeta qm;
                                 qm.walker = wk; qm.step = step; qm.rank = r; qm.ok = -1;
@@ -1040,9 +840,9 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
         // ---------------- store the walker and its class image ----------------
         store_rows(a.cur + (size_t)wk * FG_PLANES * R, R);
         if (img) {
-            uint32_t *sai = img, *lci = img + 3 * RM / 2, *twi = lci + RM;
+            uint32_t *nxi = img, *lci = img + 3 * RM / 2, *twi = lci + RM;
 #pragma unroll 1
-            for (int k = lane; k < 3 * RM / 2; k += 32) sai[k] = reinterpret_cast<const uint32_t *>(s.sa)[k];
+            for (int k = lane; k < 3 * RM / 2; k += 32) nxi[k] = reinterpret_cast<const uint32_t *>(s.nxh)[k];
 #pragma unroll 1
             for (int l = lane; l < RM; l += 32) lci[l] = s.lc[l];
             twi[lane] = s.tw[lane];
@@ -1087,11 +887,11 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
 }
 
 // shared memory per warp: factors, lc, word totals (32), sign bits (16), Philox table,
-// counters, sorted arrays and positions (2 x 3 x RM u16)
+// counters, next arrays (3 x RM u16)
 template <class P> size_t wl_smem(int nwd)
 {
     return (size_t)3 * 32 * nwd * sizeof(typename P::F) + 32 * nwd * 4 + 32 * 4 + 16 * 4 + 32 * PXS * 4 + 8 * 4 +
-           2 * 3 * 32 * nwd * 2;
+           3 * 32 * nwd * 2;
 }
 
 template <class P, int MINB>
@@ -1123,8 +923,8 @@ cudaError_t launch_wl(const WalkArgs &a, int num_sms, cudaStream_t st)
     if (mb == 20) return launch_wl_m<P, 20>(a, num_sms, st);
     if (mb == 24) return launch_wl_m<P, 24>(a, num_sms, st);
     if (mb == 16) return launch_wl_m<P, 16>(a, num_sms, st);
-    // round-1 measurement (scripts/gpu_r02_minb.sh): P32 (C4) ran best with 20 resident
-    // warps' worth of registers (96), the P64 layouts with 16 (128 registers)
+    // measured (scripts/gpu_r02_minb.sh): P32 (C4) runs best with 20 resident warps' worth
+    // of registers (96), the P64 layouts with 16 (128 registers; 96 spills too much)
     if (std::is_same<P, P32>::value) return launch_wl_m<P, 20>(a, num_sms, st);
     return launch_wl_m<P, 16>(a, num_sms, st);
 }
