@@ -397,8 +397,12 @@ int fg_create(int m, int n, int p, int ring, int r_cap, int64_t num_walkers, int
     c->stream = (cudaStream_t)cuda_stream;
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     const size_t words = (size_t)FG_PLANES * r_cap;
-    // verify queue: 8 entries per walker, at least 1024
-    c->qcap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1024, 8 * num_walkers), 1 << 22);
+    // verify queue (R19): 8 entries per walker, at least 1024, at most 512 MB of entries
+    // (strict improvements are rare after the first phases: C2 verifies ~900 per 10^4-step
+    // phase of 16384 walkers; an overflow falls back to verifying the walker's final best
+    // and is counted, fg_stats [7]; DESIGN.md section 2 "Verify-queue overflow")
+    const int64_t q_budget = (int64_t)(512ll << 20) / (int64_t)(words * sizeof(uint64_t));
+    c->qcap = (uint32_t)std::min<int64_t>(std::max<int64_t>(1024, std::min<int64_t>(8 * num_walkers, q_budget)), 1 << 22);
     int rc = FG_OK;
     auto alloc = [&](void **ptr, size_t bytes) {
         if (rc != FG_OK) return;
