@@ -32,6 +32,7 @@ struct DevMisc {         // small device-side scratch read back after every fg_w
     uint32_t pad;
     unsigned long long restarted;
     unsigned long long work_counter;
+    unsigned long long ring_tail;
     uint32_t dbgbuf[16];
 };
 
@@ -51,7 +52,8 @@ struct fg_ctx {
     fg_qmeta *d_qmeta;
     DevMisc *d_misc;
     uint32_t *d_task_done;   // walk_ql chunk flags, one per walker group of 8
-    uint32_t *d_ql_img;      // walk_ql: shared-memory image per walker between chunks
+    uint32_t *d_ql_img;      // walk_ql / walk_q4: shared-memory image per walker between chunks
+    uint32_t *d_ring;        // walk_q4: ready queue of step-chunk tasks
     uint32_t *d_wl_img;      // walk_wl: class image per walker between launches
     unsigned long long *d_rank_first;   // [FG_MAX_RCAP + 1]: first step of a verified improvement to each rank
     bool img_valid;          // d_wl_img matches the walkers' rows (cleared by every host write)
@@ -415,8 +417,12 @@ int fg_create(int m, int n, int p, int ring, int r_cap, int64_t num_walkers, int
     alloc((void **)&c->d_qmeta, sizeof(fg_qmeta) * c->qcap);
     alloc((void **)&c->d_misc, sizeof(DevMisc));
     alloc((void **)&c->d_task_done, sizeof(uint32_t) * (size_t)((num_walkers + 7) / 8 + 1));
-    if (kind == FG_K_QL_P16 || kind == FG_K_QL_Z2)   // 6 R + R / 4 slots + 5 scalars, R <= 128
-        alloc((void **)&c->d_ql_img, sizeof(uint32_t) * (size_t)(6 * 128 + 32 + 5) * num_walkers);
+    if (kind == FG_K_QL_P16 || kind == FG_K_QL_Z2)   // 5 R + R / 4 slots + 7 scalars, R <= 128
+        alloc((void **)&c->d_ql_img, sizeof(uint32_t) * (size_t)(5 * 128 + 32 + 7) * num_walkers);
+    if (kind == FG_K_Q4_P16 || kind == FG_K_Q4_Z2) {  // 352 slots + 8 scalars; <= 64 chunks per group
+        alloc((void **)&c->d_ql_img, sizeof(uint32_t) * (size_t)(352 + 8) * num_walkers);
+        alloc((void **)&c->d_ring, sizeof(uint32_t) * (size_t)((num_walkers + 7) / 8) * 64);
+    }
     if (fg_kind_is_wl(kind)) alloc((void **)&c->d_wl_img, sizeof(uint32_t) * fg_wl_img_words(r_cap) * num_walkers);
     alloc((void **)&c->d_pool, words * 8);
     alloc((void **)&c->d_rank_first, sizeof(unsigned long long) * (FG_MAX_RCAP + 1));
@@ -451,6 +457,7 @@ void fg_destroy(fg_ctx *c)
     cudaSetDevice(c->device);
     cudaFree(c->d_cur); cudaFree(c->d_best); cudaFree(c->d_hdr); cudaFree(c->d_qplanes);
     cudaFree(c->d_qmeta); cudaFree(c->d_misc); cudaFree(c->d_pool); cudaFree(c->d_task_done); cudaFree(c->d_ql_img);
+    cudaFree(c->d_ring);
     cudaFree(c->d_wl_img); cudaFree(c->d_rank_first);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
@@ -558,6 +565,8 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.work_counter = &c->d_misc->work_counter;
     a.task_done = c->d_task_done;
     a.ql_img = c->d_ql_img;
+    a.ring = c->d_ring;
+    a.ring_tail = &c->d_misc->ring_tail;
     a.wl_img = c->d_wl_img;
     // the complexity mode (R24) runs the round-1 kernels; walk_wl's layouts map to walk_wm
     int kind = c->kind;
@@ -580,7 +589,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         a.steps = chunk;
         CK(cudaMemsetAsync(&c->d_misc->best_key, 0xff, sizeof(unsigned long long), c->stream));
         CK(cudaMemsetAsync(&c->d_misc->q_count, 0, sizeof(uint32_t), c->stream));
-        CK(cudaMemsetAsync(&c->d_misc->work_counter, 0, sizeof(unsigned long long), c->stream));
+        CK(cudaMemsetAsync(&c->d_misc->work_counter, 0, 2 * sizeof(unsigned long long), c->stream));
         CK(cudaMemsetAsync(c->d_task_done, 0, sizeof(uint32_t) * (size_t)((c->W + 7) / 8 + 1), c->stream));
         CK(cudaEventRecord(c->ev0, c->stream));
         a.img_valid = c->img_valid ? 1u : 0u;

@@ -61,7 +61,9 @@ struct WalkArgs {
     uint32_t *task_done;                // walk_ql: per walker group, chunks stored (zeroed per launch)
     uint32_t chunks;                    // walk_ql: step chunks per group (set by its launcher)
     uint64_t chunk_steps;
-    uint32_t *ql_img;                   // walk_ql: per-walker shared-memory image between chunks
+    uint32_t *ql_img;                   // walk_ql / walk_q4: per-walker shared-memory image between chunks
+    uint32_t *ring;                     // walk_q4: ready queue of groups (group+1 per slot, zeroed per launch)
+    unsigned long long *ring_tail;      // walk_q4: completed chunks so far (zeroed per launch)
     uint32_t *wl_img;                   // walk_wl: per-walker class image (links, later counts) between launches
     uint32_t img_valid;                 // walk_wl: wl_img matches the walkers' current rows
     uint32_t mode;                      // 0 = Alg. 1 walk, 1 = naive-complexity minimisation (R24)
@@ -89,7 +91,7 @@ cudaError_t fg_launch_walk_wl(int kind, const WalkArgs &a, int num_sms, cudaStre
 size_t fg_wl_img_words(int R);     // walk_wl class image words per walker
 bool fg_kind_is_wl(int kind);
 cudaError_t fg_launch_walk_ql(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
-cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, cudaStream_t st);
+cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, int num_sms, cudaStream_t st);
 int fg_multi_ns(int R);
 int fg_multi_kind(int ring, int maxlen, int R);
 cudaError_t fg_launch_walk_multi(int kind, int ns, const WalkArgs &a, int num_sms, cudaStream_t st);

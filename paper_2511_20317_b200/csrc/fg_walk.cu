@@ -652,7 +652,7 @@ cudaError_t fg_launch_walk(int kind, const WalkArgs &a, int num_sms, cudaStream_
     case FG_K_W32_ZT_K32: return launch_w32<P32>(a, num_sms, st);
     case FG_K_W32_Z2_K32: return launch_w32<PZ2>(a, num_sms, st);
     case FG_K_Q4_P16:
-    case FG_K_Q4_Z2: return fg_launch_walk_q4(kind, a, st);
+    case FG_K_Q4_Z2: return fg_launch_walk_q4(kind, a, num_sms, st);
     case FG_K_QL_P16:
     case FG_K_QL_Z2: return fg_launch_walk_ql(kind, a, num_sms, st);
     case FG_K_WL_P16:

@@ -32,6 +32,7 @@
 //
 // Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
 // tests/test_gpu_parity.py, tests/test_gpu_kernels.py, tests/test_gpu_fuzz.py.
+#include <cstdlib>
 #include <type_traits>
 #include "fg_device.cuh"
 
@@ -41,6 +42,9 @@ using namespace fgd;
 #define Q4_WARPS (Q4_THREADS / 32)
 #ifndef Q4_MINB
 #define Q4_MINB 16
+#endif
+#ifndef Q4_ORDER
+#define Q4_ORDER 0             // chunked tasks: 0 = completion order (ready queue), 1 = chunk-major
 #endif
 
 namespace {
@@ -69,7 +73,54 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     const int qb = lane & 28;
     const unsigned qm = 0xFu << qb;
     uint32_t *const S = smem[threadIdx.x >> 5] + (lane >> 2);
-    const int64_t wk_raw = ((int64_t)blockIdx.x * Q4_WARPS + (threadIdx.x >> 5)) * 8 + (lane >> 2);
+    // Tasks.  Unchunked (a.chunks == 1): one warp per group of 8 walkers, the whole launch.
+    // Chunked: (group, step chunk) tasks over persistent warps.  The first n_groups tasks
+    // are the groups' chunk 0; every later task is the next chunk of the group that
+    // completed a chunk earliest (a ready queue filled in completion order), so groups
+    // migrate between the 3- and 4-warp schedulers of a population that is not a
+    // multiple of the scheduler count and all finish together.
+    const int64_t n_groups = (a.num_walkers + 7) / 8;
+    const bool chunked = a.chunks > 1;
+    const uint64_t n_tasks = chunked ? (uint64_t)n_groups * a.chunks : 0;
+#pragma unroll 1
+    for (int pass = 0;; ++pass) {
+    int64_t grp;
+    uint32_t chunk = 0;
+    if (!chunked) {
+        if (pass > 0) break;
+        grp = (int64_t)blockIdx.x * Q4_WARPS + (threadIdx.x >> 5);
+    } else {
+        unsigned long long k = 0;
+        uint32_t g1 = 0, ch = 0;
+        if (lane == 0) {
+            k = atomicAdd(a.work_counter, 1ull);
+            if (k < n_tasks) {
+                if (k < (unsigned long long)n_groups) {
+                    g1 = (uint32_t)k + 1u;
+                } else if (Q4_ORDER == 1) {
+                    // chunk-major: chunk k / n_groups of group k % n_groups, after its predecessor
+                    g1 = (uint32_t)(k % (unsigned long long)n_groups) + 1u;
+                    ch = (uint32_t)(k / (unsigned long long)n_groups);
+                    while (*(volatile uint32_t *)(a.task_done + (g1 - 1u)) < ch) __nanosleep(256);
+                    __threadfence();
+                } else {
+                    while ((g1 = *(volatile uint32_t *)(a.ring + (k - n_groups))) == 0u) __nanosleep(256);
+                    __threadfence();
+                    ch = *(volatile uint32_t *)(a.task_done + (g1 - 1u));
+                }
+            }
+        }
+        k = __shfl_sync(FULL, k, 0);
+        if (k >= n_tasks) break;
+        grp = (int64_t)__shfl_sync(FULL, g1, 0) - 1;
+        chunk = __shfl_sync(FULL, ch, 0);
+        __threadfence();
+    }
+    const bool last_chunk = chunk + 1 >= (chunked ? a.chunks : 1u);
+    const uint64_t done_steps = (uint64_t)chunk * a.chunk_steps;
+    const uint64_t left = done_steps >= a.steps ? 0 : a.steps - done_steps;
+    const uint32_t nsteps_task = (uint32_t)(!chunked ? a.steps : (last_chunk ? left : (left < a.chunk_steps ? left : a.chunk_steps)));
+    const int64_t wk_raw = grp * 8 + (lane >> 2);
     // a quad past the last walker stays in the warp (r = 0, no stores) so the main
     // loop's full-warp collectives see every lane
     const bool valid = wk_raw < a.num_walkers;
@@ -111,10 +162,29 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
     int best_adds = hp->best_adds;
 
     // ---------------- load the walker and its best (own rows) ----------------
+    // chunk 0 from the plane layout; later chunks restore the shared-memory image and the
+    // scalars the previous chunk of this launch saved (ql_img)
+    constexpr int IMGQ = Q4_SLOTS + 8;
+    uint32_t *const img = a.ql_img ? a.ql_img + (size_t)wk * IMGQ : nullptr;
+    const bool resume = chunk > 0 && img != nullptr;
     uint32_t wneg = 0, bwneg = 0;
     int nnz_cur = 0;
+    uint32_t nCp = 0;
+    bool maybe = true;     // R15: a full reduce_all may find work (SURVEY 8(d))
+    bool bdirty = false;   // best rows changed in this launch
+    if (resume && valid) {
 #pragma unroll 1
-    for (int l = q; l < 32; l += 4) {
+        for (int k = q; k < Q4_SLOTS; k += 4) S[k * 8] = img[k];
+        wneg = img[Q4_SLOTS];
+        bwneg = img[Q4_SLOTS + 1];
+        nnz_cur = (int)img[Q4_SLOTS + 2];
+        nCp = img[Q4_SLOTS + 3];
+        maybe = img[Q4_SLOTS + 4] != 0u;
+        bdirty = img[Q4_SLOTS + 5] != 0u;
+    }
+    qsync();
+#pragma unroll 1
+    for (int l = q; l < 32 && !resume; l += 4) {
         F u = 0, v = 0, w = 0, bu = 0, bv = 0, bwv = 0;
         if (l < R) {
             if (l < r) {
@@ -134,16 +204,17 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         FK(l, 0) = u; FK(l, 1) = v; FK(l, 2) = P::abs(w);
         BK(l, 0) = bu; BK(l, 1) = bv; BK(l, 2) = P::abs(bwv);
     }
-    wneg = qor(wneg);
-    bwneg = qor(bwneg);
-    nnz_cur = qsum(nnz_cur);
+    if (!resume) {
+        wneg = qor(wneg);
+        bwneg = qor(bwneg);
+        nnz_cur = qsum(nnz_cur);
+    }
     qsync();
     auto live_mask = [&]() -> uint32_t { return r >= 32 ? FULL : ((1u << r) - 1u); };
     auto above_of = [](int l) -> uint32_t { return ~((2u << l) - 1u); };
 
     // class masks and later counts of own rows from scratch (once per launch)
-    uint32_t nCp = 0;
-    {
+    if (!resume) {
         const uint32_t live = live_mask();
         uint32_t part = 0;
 #pragma unroll 1
@@ -165,8 +236,6 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         nCp = (uint32_t)qsum((int)part);
         qsync();
     }
-    bool maybe = true;     // R15: a full reduce_all may find work (SURVEY 8(d))
-    bool bdirty = false;   // best rows changed in this launch
 
     auto fac = [&](int l, int X) -> F {
         const F k = FK(l, X);
@@ -534,7 +603,7 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         }
     };
 
-    const uint32_t nsteps = (uint32_t)a.steps;        // host chunks launches below 2^31 steps
+    const uint32_t nsteps = nsteps_task;              // host chunks launches below 2^31 steps
 #pragma unroll 1
     for (uint32_t it = 0; it < nsteps; ++it, ++step) {
         // Philox (R8): lane 0 block 0 (draw 0 + Bernoulli words), lanes 1 and 3 block 2
@@ -715,10 +784,24 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         digest ^= digest >> 32;
     }
 
-    // ---------------- store own rows (and the best if it changed) ----------------
+    // ---------------- not the last chunk: save the image for the next one ----------------
+    if (!last_chunk && valid) {
+        qsync();
+#pragma unroll 1
+        for (int k = q; k < Q4_SLOTS; k += 4) img[k] = S[k * 8];
+        if (q == 0) {
+            img[Q4_SLOTS] = wneg;
+            img[Q4_SLOTS + 1] = bwneg;
+            img[Q4_SLOTS + 2] = (uint32_t)nnz_cur;
+            img[Q4_SLOTS + 3] = nCp;
+            img[Q4_SLOTS + 4] = maybe ? 1u : 0u;
+            img[Q4_SLOTS + 5] = bdirty ? 1u : 0u;
+        }
+    }
+    // ---------------- last chunk: store own rows (and the best if it changed) ----------------
     uint64_t *cw = a.cur + (size_t)wk * FG_PLANES * R;
     int best_nnz = 0;
-    for (int l = q; l < R && valid; l += 4) {
+    for (int l = q; l < R && valid && last_chunk; l += 4) {
         const bool lv = l < r;
         const F u = lv ? FK(l, 0) : 0, v = lv ? FK(l, 1) : 0, w = lv ? fac(l, 2) : 0;
         cw[0 * R + l] = P::dig(u); cw[1 * R + l] = P::sgn(u);
@@ -741,10 +824,10 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         hp->step = step;
         hp->digest = digest;
         hp->best_adds = best_adds;
-        hp->cnt[FG_CNT_STEPS] += a.steps;
+        hp->cnt[FG_CNT_STEPS] += nsteps_task;
         hp->cnt[FG_CNT_DRAWS] += c_draws;
         hp->cnt[FG_CNT_FLIPS] += c_flips;
-        hp->cnt[FG_CNT_FLIP_FAIL] += a.steps - c_flips;
+        hp->cnt[FG_CNT_FLIP_FAIL] += nsteps_task - c_flips;
         hp->cnt[FG_CNT_EXPAND_OK] += c_eok;
         hp->cnt[FG_CNT_EXPAND_REJECT] += c_erej;
         hp->cnt[FG_CNT_MERGES] += c_merge;
@@ -754,9 +837,25 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
         hp->cnt[FG_CNT_REDUCE_CALLS] += c_red;
         int adds = best_nnz - 2 * best - a.mp;
         if (adds < 0) adds = 0;
-        atomicMin(a.best_key, ((unsigned long long)best << 54) | ((unsigned long long)adds << 36) |
-                                  (unsigned long long)wk);
+        if (last_chunk)
+            atomicMin(a.best_key, ((unsigned long long)best << 54) | ((unsigned long long)adds << 36) |
+                                      (unsigned long long)wk);
     }
+    // chunk stored: publish the group's next chunk in the ready queue
+    if (chunked && !last_chunk) {
+        __syncwarp();
+        __threadfence();
+        if (lane == 0) {
+            atomicExch(a.task_done + grp, chunk + 1u);
+            __threadfence();
+            if (Q4_ORDER == 0) {
+                const unsigned long long slot = atomicAdd(a.ring_tail, 1ull);
+                atomicExch(a.ring + slot, (uint32_t)grp + 1u);
+            }
+        }
+    }
+    __syncwarp();
+    }   // task loop
 #undef FK
 #undef MK
 #undef LK
@@ -764,25 +863,51 @@ __global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
 #undef BK
 }
 
-template <class P>
-cudaError_t launch_q4(const WalkArgs &a, cudaStream_t st)
+template <class P, bool CM>
+cudaError_t launch_q4_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
-    const int64_t per_block = Q4_WARPS * 8;
-    const int64_t blocks = (a.num_walkers + per_block - 1) / per_block;
-    if (a.mode == 1)
-        walk_q4<P, true><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(a);
-    else
-        walk_q4<P, false><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(a);
+    const int64_t groups = (a.num_walkers + 7) / 8;
+    int bps = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_q4<P, CM>, Q4_THREADS, 0);
+    if (e != cudaSuccess) return e;
+    if (bps < 1) bps = 1;
+    const int64_t resident = (int64_t)num_sms * bps * Q4_WARPS;     // warps
+    WalkArgs b = a;
+    // chunked tasks when the population gives every scheduler more than one warp but is
+    // not a whole number of warps per scheduler (the C2 case: 2048 warps on 592
+    // schedulers); FG_Q4_CHUNKS forces a count (tests, A/B)
+    b.chunks = (groups > (int64_t)num_sms * 4 && groups <= resident && a.steps >= 512 && a.ql_img && a.ring) ? 8u : 1u;
+    if (const char *ev = getenv("FG_Q4_CHUNKS")) {
+        const long k = strtol(ev, nullptr, 10);
+        if (k >= 1 && k <= 64 && a.ql_img && a.ring) b.chunks = (uint32_t)k;
+    }
+    if ((uint64_t)b.chunks > a.steps) b.chunks = a.steps > 0 ? (uint32_t)a.steps : 1u;
+    b.chunk_steps = (a.steps + b.chunks - 1) / b.chunks;
+    int64_t blocks;
+    if (b.chunks > 1) {
+        e = cudaMemsetAsync(b.ring, 0, sizeof(uint32_t) * (size_t)(groups * b.chunks), st);
+        if (e != cudaSuccess) return e;
+        blocks = resident / Q4_WARPS;
+    } else {
+        blocks = (groups + Q4_WARPS - 1) / Q4_WARPS;
+    }
+    walk_q4<P, CM><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(b);
     return cudaGetLastError();
+}
+
+template <class P>
+cudaError_t launch_q4(const WalkArgs &a, int num_sms, cudaStream_t st)
+{
+    return a.mode == 1 ? launch_q4_m<P, true>(a, num_sms, st) : launch_q4_m<P, false>(a, num_sms, st);
 }
 
 }  // namespace
 
-cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, cudaStream_t st)
+cudaError_t fg_launch_walk_q4(int kind, const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     switch (kind) {
-    case FG_K_Q4_P16: return launch_q4<P16>(a, st);
-    case FG_K_Q4_Z2: return launch_q4<PZ2>(a, st);
+    case FG_K_Q4_P16: return launch_q4<P16>(a, num_sms, st);
+    case FG_K_Q4_Z2: return launch_q4<PZ2>(a, num_sms, st);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -228,3 +228,31 @@ def test_wl_large_classes(fg, orc, case):
     got = g.get_walkers()
     ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
     _check(got, ref, None)
+
+
+@pytest.mark.parametrize("case", [((3, 3, 3), ZT, 32, 203, 2600, "5"), ((3, 3, 3), Z2, 32, 517, 1800, "7"),
+                                  ((2, 2, 2), ZT, 12, 64, 3000, "4"), ((3, 3, 3), ZT, 32, 1000, 900, "64")],
+                         ids=lambda c: f"{c[0]}-{'zt' if c[1] == ZT else 'z2'}-W{c[3]}-C{c[5]}")
+def test_q4_chunked_tasks(fg, orc, case):
+    """walk_q4's completion-ordered (walker group, step chunk) tasks (FG_Q4_CHUNKS forces
+    the chunk count; the C2 bench configuration chunks by default): every trajectory is
+    unchanged, across two launches, with ragged chunk lengths and a count above the
+    steps of a launch (64 chunks of a 450-step launch)."""
+    (m, n, p), ring, R, W, steps, chunks = case
+    seed = 0xC5C5 + W
+    old = os.environ.get("FG_Q4_CHUNKS")
+    os.environ["FG_Q4_CHUNKS"] = chunks
+    try:
+        g = _ctx(fg, "q4", m, n, p, ring, R, W)
+        g.seed_naive()
+        g.walk(steps, seed, fg.params_default(phase_steps=steps // 2))
+    finally:
+        if old is None:
+            del os.environ["FG_Q4_CHUNKS"]
+        else:
+            os.environ["FG_Q4_CHUNKS"] = old
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ring, R, W, 0, steps, seed)
+    _check(got, ref, None)
+    assert np.all(got["step"] == steps)
+    assert g.stats()["verify_fail"] == 0
