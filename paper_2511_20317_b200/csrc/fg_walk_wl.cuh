@@ -106,7 +106,7 @@ __device__ __noinline__ int key_change(WS<P> s, int r, int t, int X, typename P:
     int pO = NIL, sO = NIL, pK = NIL, sK = NIL, aK = 0, tO = 0, tK = 0;
     const F *fx = s.fac + X * s.RM;
 #pragma unroll 1
-    for (int w = 0; w < s.nwd; ++w) {
+    for (int w = 0; w < ((r + 31) >> 5); ++w) {        // live words only
         const int l = 32 * w + lane;
         const F x = fx[l];
         const bool live = l < r && l != t;
@@ -186,7 +186,7 @@ __device__ __noinline__ Found<P> first_reducible(WS<P> s, int r, int t, int lmin
     out.j = -1;
     out.mg = rt;
 #pragma unroll 1
-    for (int w = 0; w < s.nwd; ++w) {
+    for (int w = 0; w < ((r + 31) >> 5); ++w) {
         const int l = 32 * w + lane;
         const int c = (int)P::eq(s.key(0, l), k0) + (int)P::eq(s.key(1, l), k1) + (int)P::eq(s.key(2, l), k2);
         uint32_t m = __ballot_sync(FULL, l < r && l != t && l >= lmin && c >= 2);
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             for (;;) {
                 int zfirst = -1;
 #pragma unroll 1
-                for (int w = 0; w < nwd && zfirst < 0; ++w) {
+                for (int w = 0; w < ((r + 31) >> 5) && zfirst < 0; ++w) {
                     const int l = 32 * w + lane;
                     const uint32_t m = __ballot_sync(FULL, l < r && row_zero(l));
                     if (m) zfirst = 32 * w + __ffs(m) - 1;
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                 // per scheduler: +2 % on C5); one for P32 (-2 % on C4, scripts/gpu_r02_ab.sh)
                 constexpr int PASS_UNROLL = sizeof(F) > 8 ? 2 : 1;
 #pragma unroll PASS_UNROLL
-                for (int w = 0; w < nwd; ++w) {
+                for (int w = 0; w < ((r + 31) >> 5); ++w) {        // live words only
                     const int l = 32 * w + lane;
                     const F xX = pX[l], xY = pY[l], xZ = pZ[l];
                     const bool la = l < r && l != alpha, lb = l < r && l != beta;
