@@ -51,11 +51,11 @@ def parse():
 # (kernel, workload) -> (dram bytes per launch, profile it comes from)
 # and the capture's issue / ALU-pipe utilisation (the north star's "% int-issue" figures)
 NCU_TRAFFIC = {
-    ("walk_q4<P16>", "c2_333_zt"): (52.887808e6 + 5.603584e6, "profiles/r02_ncu_walk_q4_c2_333_zt.txt", 58.90, 50.5),
-    ("walk_ql<P16>", "c3_444_zt"): (74.933248e6 + 59.2576e6, "profiles/r02_ncu_walk_ql_c3_444_zt.txt", 51.53, 51.0),
+    ("walk_q4<P16>", "c2_333_zt"): (54.318592e6 + 27.93728e6, "profiles/r02_ncu_walk_q4_c2_333_zt.txt", 56.17, 50.2),
+    ("walk_ql<P16>", "c3_444_zt"): (74.864128e6 + 59.28576e6, "profiles/r02_ncu_walk_ql_c3_444_zt.txt", 52.05, 51.5),
     ("walk_ql<PZ2>", "c3_444_z2"): (49.468416e6 + 51.462656e6, "profiles/r02_ncu_walk_ql_c3_444_z2.txt", 53.40, 53.5),
-    ("walk_wl<P32>", "c4_555_zt"): (179.79392e6 + 143.013632e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 73.68, 73.3),
-    ("walk_wl<P64>", "c5_679_zt"): (310.194944e6 + 186.071296e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 42.84, 55.2),
+    ("walk_wl<P32>", "c4_555_zt"): (181.10592e6 + 137.518336e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 73.82, 72.6),
+    ("walk_wl<P64>", "c5_679_zt"): (308.32e6 + 184.611584e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 42.90, 56.3),
 }
 
 

@@ -25,7 +25,7 @@ class PoolSync:
         """All-gather one uint8 record per rank; returns world x bytes."""
         import torch
         import torch.distributed as dist
-        if self.world == 1:
+        if self.world == 1 and not dist.is_initialized():
             return rec.reshape(1, -1)
         backend = dist.get_backend(self.group)
         dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
@@ -37,7 +37,8 @@ class PoolSync:
     def exchange(self) -> dict:
         """Export the local best, all-gather, merge into the pool; returns the
         box-wide best (rank, additions, walker id, coeffs)."""
-        if self.world > 1:
+        import torch.distributed as dist
+        if self.world > 1 or dist.is_initialized():
             recs = self.gather_records(self.g.export_best())
             self.g.import_best(np.ascontiguousarray(recs.reshape(-1)), self.world)
         return self.g.best()
