@@ -41,7 +41,7 @@ using namespace fgd;
 #define Q4_THREADS 32
 #define Q4_WARPS (Q4_THREADS / 32)
 #ifndef Q4_MINB
-#define Q4_MINB 16
+#define Q4_MINB 14             // 146 registers: no spills; 14 warps x 148 SMs >= the C2 population (2048 warps)
 #endif
 #ifndef Q4_ORDER
 #define Q4_ORDER 0             // chunked tasks: 0 = completion order (ready queue), 1 = chunk-major
