@@ -180,9 +180,13 @@ int fg_restart(fg_ctx *ctx, int slack, int64_t *restarted);
 
 /* Checkpoint / resume and host-buffer I/O: the complete walker state (planes of
    current and best schemes, ranks, step indices, digests, counters) as an opaque
-   byte image of fg_state_bytes(ctx) bytes (64-byte header, walker headers, current
-   and best planes, and for the linked-class kernel walk_wl its per-walker class
-   image).  Resuming from it continues every trajectory bit-exactly (R8). */
+   byte image of fg_state_bytes(ctx) bytes (64-byte header whose word 10 is the bytes
+   per plane word, walker headers, current and best planes packed to 2 / 4 / 8 bytes
+   per plane word for factors of <= 16 / 32 / 64 elements, and for the linked-class
+   kernel walk_wl its per-walker class image).  Packing and unpacking run on the device
+   around one copy each way.  Resuming from it continues every trajectory bit-exactly
+   (R8).  fg_load_state rejects an image of another format, ring, capacity, walker
+   count or plane width (FG_E_ARG). */
 size_t fg_state_bytes(const fg_ctx *ctx);
 int fg_save_state(const fg_ctx *ctx, void *host_buf);
 int fg_load_state(fg_ctx *ctx, const void *host_buf);

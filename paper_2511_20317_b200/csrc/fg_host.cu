@@ -13,7 +13,7 @@
 namespace {
 
 constexpr uint32_t REC_MAGIC = 0x46475231u;   // "FGR1"
-constexpr uint32_t STATE_MAGIC = 0x46475331u; // "FGS1"
+constexpr uint32_t STATE_MAGIC = 0x46475332u; // "FGS2": planes packed to the factor width
 
 struct RecHdr {          // 64 bytes, followed by 6*r_cap u64 planes
     uint32_t magic;
@@ -55,6 +55,7 @@ struct fg_ctx {
     uint32_t *d_ql_img;      // walk_ql / walk_q4: shared-memory image per walker between chunks
     uint32_t *d_ring;        // walk_q4: ready queue of step-chunk tasks
     uint32_t *d_wl_img;      // walk_wl: class image per walker between launches
+    void *d_stage = nullptr; // fg_save_state / fg_load_state: packed planes (lazily allocated)
     unsigned long long *d_rank_first;   // [FG_MAX_RCAP + 1]: first step of a verified improvement to each rank
     bool img_valid;          // d_wl_img matches the walkers' rows (cleared by every host write)
     uint32_t qcap;
@@ -346,6 +347,51 @@ int recompute_local_best(fg_ctx *c)
 
 }  // namespace
 
+// host-buffer state I/O: every plane word holds at most maxlen <= 64 significant bits,
+// so the current and best planes travel packed to 2, 4 or 8 bytes per word (C2: 12 of
+// 48 bytes per row); a device kernel packs / unpacks around one copy each way
+static int plane_width(const fg_ctx *c) { return c->maxlen <= 16 ? 2 : (c->maxlen <= 32 ? 4 : 8); }
+
+template <class T>
+__global__ void pack_planes_kernel(const uint64_t *a, const uint64_t *b, T *out, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = (T)(i < n ? a[i] : b[i - n]);
+}
+template <class T>
+__global__ void unpack_planes_kernel(const T *in, uint64_t *a, uint64_t *b, int64_t n)
+{
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 2 * n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = (uint64_t)in[i];
+        if (i < n) a[i] = v; else b[i - n] = v;
+    }
+}
+
+static int stage_planes(const fg_ctx *cc, bool pack)
+{
+    fg_ctx *c = const_cast<fg_ctx *>(cc);
+    const int64_t n = (int64_t)FG_PLANES * c->R * c->W;
+    const int bw = plane_width(c);
+    if (!c->d_stage && cudaMalloc(&c->d_stage, (size_t)(2 * n * bw)) != cudaSuccess) {
+        c->d_stage = nullptr;
+        return FG_E_CUDA;
+    }
+    const int64_t blocks = std::min<int64_t>((2 * n + 255) / 256, (int64_t)c->num_sms * 16);
+    if (bw == 2) {
+        if (pack) pack_planes_kernel<uint16_t><<<(unsigned)blocks, 256, 0, c->stream>>>(c->d_cur, c->d_best, (uint16_t *)c->d_stage, n);
+        else unpack_planes_kernel<uint16_t><<<(unsigned)blocks, 256, 0, c->stream>>>((const uint16_t *)c->d_stage, c->d_cur, c->d_best, n);
+    } else if (bw == 4) {
+        if (pack) pack_planes_kernel<uint32_t><<<(unsigned)blocks, 256, 0, c->stream>>>(c->d_cur, c->d_best, (uint32_t *)c->d_stage, n);
+        else unpack_planes_kernel<uint32_t><<<(unsigned)blocks, 256, 0, c->stream>>>((const uint32_t *)c->d_stage, c->d_cur, c->d_best, n);
+    } else {
+        if (pack) pack_planes_kernel<uint64_t><<<(unsigned)blocks, 256, 0, c->stream>>>(c->d_cur, c->d_best, (uint64_t *)c->d_stage, n);
+        else unpack_planes_kernel<uint64_t><<<(unsigned)blocks, 256, 0, c->stream>>>((const uint64_t *)c->d_stage, c->d_cur, c->d_best, n);
+    }
+    c->st_launches++;
+    CK(cudaGetLastError());
+    return FG_OK;
+}
+
 extern "C" {
 
 void fg_params_default(fg_params *o)
@@ -457,7 +503,7 @@ void fg_destroy(fg_ctx *c)
     cudaSetDevice(c->device);
     cudaFree(c->d_cur); cudaFree(c->d_best); cudaFree(c->d_hdr); cudaFree(c->d_qplanes);
     cudaFree(c->d_qmeta); cudaFree(c->d_misc); cudaFree(c->d_pool); cudaFree(c->d_task_done); cudaFree(c->d_ql_img);
-    cudaFree(c->d_ring);
+    cudaFree(c->d_ring); cudaFree(c->d_stage);
     cudaFree(c->d_wl_img); cudaFree(c->d_rank_first);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
@@ -897,7 +943,7 @@ size_t fg_state_bytes(const fg_ctx *c)
 {
     if (!c) return 0;
     const size_t words = (size_t)FG_PLANES * c->R;
-    return 64 + sizeof(fg_whdr) * c->W + 2 * words * 8 * c->W + img_bytes(c);
+    return 64 + sizeof(fg_whdr) * c->W + 2 * words * plane_width(c) * c->W + img_bytes(c);
 }
 
 int fg_save_state(const fg_ctx *c, void *buf)
@@ -906,17 +952,20 @@ int fg_save_state(const fg_ctx *c, void *buf)
     if (!c->seeded) return FG_E_STATE;
     CK(cudaSetDevice(c->device));
     const size_t words = (size_t)FG_PLANES * c->R;
+    const size_t pb = 2 * words * plane_width(c) * c->W;
     unsigned char *b = (unsigned char *)buf;
     const size_t ib = img_bytes(c);
     uint32_t hdr[16] = {STATE_MAGIC, (uint32_t)c->m, (uint32_t)c->n, (uint32_t)c->p, (uint32_t)c->ring,
                         (uint32_t)c->R, (uint32_t)(c->W & 0xffffffff), (uint32_t)(c->W >> 32),
-                        (uint32_t)(ib ? fg_wl_img_words(c->R) : 0), (uint32_t)(ib && c->img_valid)};
+                        (uint32_t)(ib ? fg_wl_img_words(c->R) : 0), (uint32_t)(ib && c->img_valid),
+                        (uint32_t)plane_width(c)};
     memcpy(b, hdr, 64);
+    const int rc = stage_planes(c, true);
+    if (rc != FG_OK) return rc;
     CK(cudaMemcpyAsync(b + 64, c->d_hdr, sizeof(fg_whdr) * c->W, cudaMemcpyDeviceToHost, c->stream));
     unsigned char *pc = b + 64 + sizeof(fg_whdr) * c->W;
-    CK(cudaMemcpyAsync(pc, c->d_cur, words * 8 * c->W, cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaMemcpyAsync(pc + words * 8 * c->W, c->d_best, words * 8 * c->W, cudaMemcpyDeviceToHost, c->stream));
-    if (ib) CK(cudaMemcpyAsync(pc + 2 * words * 8 * c->W, c->d_wl_img, ib, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(pc, c->d_stage, pb, cudaMemcpyDeviceToHost, c->stream));
+    if (ib) CK(cudaMemcpyAsync(pc + pb, c->d_wl_img, ib, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     return FG_OK;
 }
@@ -927,19 +976,25 @@ int fg_load_state(fg_ctx *c, const void *buf)
     const uint32_t *hdr = (const uint32_t *)buf;
     if (hdr[0] != STATE_MAGIC || (int)hdr[1] != c->m || (int)hdr[2] != c->n || (int)hdr[3] != c->p ||
         (int)hdr[4] != c->ring || (int)hdr[5] != c->R ||
-        ((int64_t)hdr[6] | ((int64_t)hdr[7] << 32)) != c->W)
+        ((int64_t)hdr[6] | ((int64_t)hdr[7] << 32)) != c->W || (int)hdr[10] != plane_width(c))
         return FG_E_ARG;
     CK(cudaSetDevice(c->device));
     const size_t words = (size_t)FG_PLANES * c->R;
+    const size_t pb = 2 * words * plane_width(c) * c->W;
     const unsigned char *b = (const unsigned char *)buf;
+    if (!c->d_stage && cudaMalloc(&c->d_stage, pb) != cudaSuccess) {
+        c->d_stage = nullptr;
+        return FG_E_CUDA;
+    }
     CK(cudaMemcpyAsync(c->d_hdr, b + 64, sizeof(fg_whdr) * c->W, cudaMemcpyHostToDevice, c->stream));
     const unsigned char *pc = b + 64 + sizeof(fg_whdr) * c->W;
-    CK(cudaMemcpyAsync(c->d_cur, pc, words * 8 * c->W, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpyAsync(c->d_best, pc + words * 8 * c->W, words * 8 * c->W, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->d_stage, pc, pb, cudaMemcpyHostToDevice, c->stream));
+    const int rc = stage_planes(c, false);
+    if (rc != FG_OK) return rc;
     // a class image saved by the same kind of context resumes as it was saved
     const size_t ib = img_bytes(c);
     const bool img = ib && hdr[8] == (uint32_t)fg_wl_img_words(c->R) && hdr[9] == 1u;
-    if (img) CK(cudaMemcpyAsync(c->d_wl_img, pc + 2 * words * 8 * c->W, ib, cudaMemcpyHostToDevice, c->stream));
+    if (img) CK(cudaMemcpyAsync(c->d_wl_img, pc + pb, ib, cudaMemcpyHostToDevice, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     c->covered.assign(1, {0, c->W});
     c->img_valid = img;

@@ -179,8 +179,11 @@ HDR = 128          # fg_whdr bytes: r, best_r, step, digest, cnt[12], best_adds,
 
 
 def _state_views(buf, W, R):
+    """Views of fg_save_state's image (include/fg.h): 64-byte header (word 10 = bytes per
+    plane word), walker headers, then the current and the best planes packed to that width."""
+    bw = int(np.frombuffer(bytes(buf[40:44]), np.uint32)[0])
     hdr = buf[64: 64 + HDR * W].reshape(W, HDR)
-    words = 6 * R * 8
+    words = 6 * R * bw
     cur = buf[64 + HDR * W: 64 + HDR * W + words * W].reshape(W, words)
     best = buf[64 + HDR * W + words * W: 64 + HDR * W + 2 * words * W].reshape(W, words)
     return hdr, cur, best
@@ -201,7 +204,7 @@ def test_unverified_best_never_becomes_the_local_best(fg, orc):
     k = (good["walker_id"] + 1) % W
     hdr[k, 4:8] = np.frombuffer(np.int32(5).tobytes(), np.uint8)      # best_r = 5: beats everyone
     best[k, :] = 0
-    best[k, :8] = 1                                                    # not a scheme
+    best[k, :1] = 1                                                    # not a scheme
     b = _ctx(fg, 3, 3, 3, ZT, R, W)
     with pytest.raises(fg.FgError) as e:
         b.load_state(img)
