@@ -20,4 +20,9 @@ for spec in ${PROF:-c2_333_zt:10000 c3_444_zt:2000 c4_555_zt:2000 c5_679_zt:2000
   timeout 300 $B > $O.plain_$wl.json 2> $O.plain_$wl.err || continue
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:walk_ -s 1 -c 1 \
     -o $O.full_$wl -f $B > $O.ncu_$wl.log 2>&1; echo "ncu rc=$?" >> $O.ncu_$wl.log
+  # summary on the box (walker-steps per launch from the plain run's config); the report
+  # itself comes back only with KEEP_REPS (gpurun_out returns at most 64 MiB)
+  ws=$(python -c "import json; d=json.loads(open('$O.plain_$wl.json').read().strip().splitlines()[-1]); print(d['config']['walkers_per_gpu']*d['config']['phase_steps'])")
+  python tools/ncu_summary.py $O.full_$wl.ncu-rep $ws > $O.sum_$wl.txt 2>&1
+  [ -z "$KEEP_REPS" ] && rm -f $O.full_$wl.ncu-rep
 done

@@ -9,7 +9,7 @@ import subprocess
 import sys
 
 KEYS = ["gpu__time_duration.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
-        "sm__inst_executed.sum", "smsp__warps_active.avg.per_cycle_active",
+        "sm__inst_executed.sum", "smsp__inst_executed.sum", "smsp__warps_active.avg.per_cycle_active",
         "smsp__warps_eligible.avg.per_cycle_active", "launch__registers_per_thread",
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "dram__bytes_read.sum", "dram__bytes_write.sum"]
