@@ -417,6 +417,17 @@ def main():
 
     best = g.best()
     stats = {k: st1[k] - st0[k] for k in ("verified", "verify_fail", "queue_overflow")}
+    # attempts per step and accepted flips per second (box-wide: summed over ranks)
+    cnt = torch.tensor([float(st1[k] - st0[k]) for k in ("steps", "draws", "flips", "expands", "reductions")],
+                       dtype=torch.float64, device=rdev)
+    if world > 1:
+        dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    c_steps, c_draws, c_flips, c_exp, c_red = (float(x) for x in cnt.tolist())
+    walk_stats = {"draws_per_step": c_draws / max(1.0, c_steps),
+                  "flips_accepted_per_s": c_flips / (total_ms / 1000.0),
+                  "flip_accept_rate": c_flips / max(1.0, c_steps),
+                  "expands_per_step": c_exp / max(1.0, c_steps),
+                  "reductions_per_step": c_red / max(1.0, c_steps)}
     g.close()
     pc = None
     if rank == 0 and world == 1 and not args.no_per_config:
@@ -436,7 +447,7 @@ def main():
                "time_to_rank_basis": "exact: first step index of a verified strict improvement "
                                      "(fg_rank_first_steps), device time interpolated within its phase",
                "best": {"rank": best["rank"], "additions": best["additions"]},
-               "verify": stats, "per_config": pc}
+               "verify": stats, "walk_stats": walk_stats, "per_config": pc}
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
