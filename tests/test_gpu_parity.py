@@ -360,8 +360,9 @@ def test_api_errors_and_stats(fg, orc):
 
 def test_c2_bench_launch_configuration(fg, orc):
     """The launch configuration bench.py times (C2: 16384 walkers, 10^4-step phases, the
-    default kernel), two phases; 24 sampled trajectories bit-exact, every final and
-    best scheme of a 1-in-16 sample satisfies the Brent equations on the device."""
+    default kernel with its step-chunk tasks), two phases; 256 sampled trajectories
+    bit-exact, every final and best scheme of a 1-in-16 sample satisfies
+    the Brent equations on the device."""
     wl = WORKLOADS["c2_333_zt"]
     W, steps = wl.walkers, 20000
     g = _ctx(fg, 3, 3, 3, ZT, wl.r_cap, W)
@@ -369,7 +370,7 @@ def test_c2_bench_launch_configuration(fg, orc):
     p = fg.params_default(phase_steps=10000)
     g.walk(steps, wl.seed, p)
     got = g.get_walkers()
-    ids = sample_walkers(W, 24, seed=2025)
+    ids = sample_walkers(W, 256, seed=2025)
     ref = orc.run_walkers(3, 3, 3, ZT, wl.r_cap, 0, 0, steps, wl.seed, ids=ids)
     _assert_same(got, ref, idx=ids, what="c2-bench")
     st = g.stats()
@@ -379,6 +380,22 @@ def test_c2_bench_launch_configuration(fg, orc):
     assert np.all(ok == 1)
     ok, _ = g.verify_batch([got["best"][k][: got["best_r"][k]] for k in sample])
     assert np.all(ok == 1)
+
+
+@pytest.mark.parametrize("ring", [ZT, Z2])
+def test_c2_every_walker(fg, orc, ring):
+    """C2 at full size, EVERY one of the 16384 walkers (digest, ranks, counters, current
+    and best rows) against the oracle over two 600-step launches of the default kernel
+    (chunked tasks: 16384 walkers give the 592 schedulers 3-4 warps each)."""
+    wl = WORKLOADS["c2_333_zt"]
+    W, steps = wl.walkers, 1200
+    g = _ctx(fg, 3, 3, 3, ring, wl.r_cap, W)
+    g.seed_naive()
+    g.walk(steps, wl.seed + 7 * ring, fg.params_default(phase_steps=600))
+    got = g.get_walkers()
+    ref = orc.run_walkers(3, 3, 3, ring, wl.r_cap, W, 0, steps, wl.seed + 7 * ring)
+    _assert_same(got, ref, idx=None, what="c2-all")
+    assert g.stats()["verify_fail"] == 0
 
 
 def test_virtual_ranks_match_single_gpu(fg):
