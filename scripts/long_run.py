@@ -4,7 +4,11 @@ phases from naive seeds (no restarts, no Resize); the ladder is exact (verified 
 improvements' step indices, fg_rank_first_steps), the best scheme is re-verified on the
 host (fg_verify, exact integer Brent check) and written with its invariants.
 
-  python scripts/long_run.py <workload> <seconds> <out.json>
+  python scripts/long_run.py <workload> <seconds> <out.json> [restart_every_phases slack]
+
+With a restart period, every that many phases the box-wide best becomes the pool
+(fg_export_best -> fg_import_best) and walkers whose best rank exceeds it by more than
+`slack` are re-seeded from it (fg_restart, R23; PAPER:290 population synchronisation).
 """
 import json
 import os
@@ -23,6 +27,9 @@ from paper_2511_20317_b200.inputs import WORKLOADS  # noqa: E402
 
 def main():
     key, budget, out = sys.argv[1], float(sys.argv[2]), sys.argv[3]
+    every = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+    slack = int(sys.argv[5]) if len(sys.argv) > 5 else 2
+    restarted = 0
     wl = WORKLOADS[key]
     S = 10000 if wl.r_cap <= 32 else PHASE_MULTI
     stream = torch.cuda.current_stream()
@@ -37,6 +44,9 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         phase_ms.append(e0.elapsed_time(e1))
+        if every and len(phase_ms) % every == 0:
+            g.import_best(g.export_best(), 1)
+            restarted += g.restart(slack)
         if len(phase_ms) % 25 == 1:
             b = g.best()
             trace.append({"device_s": round(sum(phase_ms) / 1000.0, 3), "best_rank": b["rank"],
@@ -51,7 +61,7 @@ def main():
     res = {"workload": wl.name, "walkers": wl.walkers, "phase_steps": S, "phases": len(phase_ms),
            "device_s": round(sum(phase_ms) / 1000.0, 3), "wall_s": round(time.time() - t0, 1),
            "walker_steps_per_s": wl.walkers * S * len(phase_ms) / (sum(phase_ms) / 1000.0),
-           "kernel": g.kernel_name,
+           "kernel": g.kernel_name, "restart": {"every_phases": every, "slack": slack, "restarted": restarted},
            "time_to_rank_s": {str(k): round(v[0], 4) for k, v in sorted(lad.items())},
            "steps_to_rank": {str(k): v[1] for k, v in sorted(lad.items())},
            "best": {"rank": b["rank"], "additions": b["additions"], "walker_id": b["walker_id"],
