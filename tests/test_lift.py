@@ -81,3 +81,22 @@ def test_budget_and_domain(fg, orc):
     bad = orc.naive(2, 2, 2)
     bad[0, 0] = -1
     assert fg.fg_lift(2, 2, 2, bad)[0] == -3
+
+
+def test_parity_system_decides_dense_cases(fg, orc):
+    """The GF(2) parity constraints (R32): on dense (3,3,3) Z_2 walk outputs the search
+    ends quickly either way -- a lift that the oracle's Brent check accepts with the same
+    support, or a proof that none exists -- where round 1's plain search ran out of its
+    budget."""
+    outcomes = set()
+    for wid in range(6):
+        w = orc.walker(3, 3, 3, 1, 32, walker_id=wid)
+        w.seed_naive()
+        w.walk(30000, 11)
+        z = w.rows(1)
+        rc, out, nodes = fg.fg_lift(3, 3, 3, z, 1_000_000)
+        assert rc in (0, -4) and nodes < 1_000_000
+        if rc == 0:
+            assert orc.verify(3, 3, 3, 0, out)[0] == 0 and np.array_equal(np.abs(out), z)
+        outcomes.add(rc)
+    assert outcomes == {0, -4}
