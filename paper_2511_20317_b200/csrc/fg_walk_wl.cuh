@@ -593,35 +593,42 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             int fY = 0, fZ = 0;
             F fny = P::make(0, 0), fnz = fny;
 
-            // ---- R11 try_flip: sequential draws over 4|C| (R9) ----
+            // ---- R11 try_flip: draws over 4|C| (R9), two at a time: half h of the warp
+            // (16 lanes) evaluates draw 2t + h; the first valid one in draw order is the one
+            // the sequential loop commits (draws are addressed, not consumed) ----
             if (nC) {
+                const int h = lane >> 4, hl = lane & 15, hb = lane & 16;
                 // prefix of the word totals, once per step (the list is not rebuilt between
-                // draws): lane w holds the inclusive sums of words 0..w, 3 x 21-bit fields
+                // draws): lane hl of each half holds the inclusive sums of words 0..hl,
+                // 3 x 21-bit fields
                 uint64_t tv = 0;
-                if (lane < nwd) {
-                    const uint32_t t0 = s.tw[lane], t1 = s.tw[16 + lane];
+                if (hl < nwd) {
+                    const uint32_t t0 = s.tw[hl], t1 = s.tw[16 + hl];
                     tv = (uint64_t)(t0 & 0xFFFFu) | ((uint64_t)(t0 >> 16) << 21) | ((uint64_t)t1 << 42);
                 }
                 uint64_t inc = tv;
 #pragma unroll
                 for (int o = 1; o < 16; o <<= 1) {
-                    const uint64_t t = __shfl_up_sync(FULL, inc, o);
-                    if (lane >= o) inc += t;
+                    const uint64_t t = __shfl_up_sync(FULL, inc, o, 16);
+                    if (hl >= o) inc += t;
                 }
                 const uint64_t exc = inc - tv;
-                uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0;
+                uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, cb = 0xFFFFFFFFu;
 #pragma unroll 1
-                for (uint32_t at = 0; at < kf; ++at) {
+                for (uint32_t at = 0; at < kf; at += 2) {
+                    const uint32_t a2 = at + (uint32_t)h;               // this half's draw
                     uint32_t x;
-                    if (at == 0) x = pw[0];
-                    else if (at <= 4) x = pw[3 + at];
+                    if (a2 == 0) x = pw[0];
+                    else if (a2 <= 4) x = pw[3 + a2];
                     else {
-                        const uint32_t slot = 7 + at;
-                        if ((slot & 3) == 0) philox_block(seed, step, wid, slot >> 2, e0, e1, e2, e3);
+                        const uint32_t slot = 7 + a2, blk = slot >> 2;
+                        if (blk != cb) {
+                            philox_block(seed, step, wid, blk, e0, e1, e2, e3);
+                            cb = blk;
+                        }
                         const uint32_t ws = slot & 3;
                         x = ws == 0 ? e0 : (ws == 1 ? e1 : (ws == 2 ? e2 : e3));
                     }
-                    draws++;
                     const uint32_t k = __umulhi(x, 4u * nC);
                     const uint32_t idx = k >> 2;
                     const int d = k & 1, e = (k >> 1) & 1;
@@ -630,31 +637,37 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
                     // the word holding row i
                     const int sh = 21 * X;
-                    const int wsel = __ffs(__ballot_sync(FULL, lane < nwd && ((uint32_t)(inc >> sh) & 0x1FFFFFu) > qq)) - 1;
-                    const uint32_t q1 = qq - ((uint32_t)(__shfl_sync(FULL, exc, wsel) >> sh) & 0x1FFFFFu);
-                    // row i inside the word: scan of its later counts
-                    const int lw = 32 * wsel + lane;
-                    const uint32_t lv = lw < r ? (uint32_t)getf(s.lc[lw], X) : 0u;
-                    uint32_t inc2 = lv;
+                    const uint32_t wb = __ballot_sync(FULL, hl < nwd && ((uint32_t)(inc >> sh) & 0x1FFFFFu) > qq);
+                    const int wsel = __ffs((wb >> hb) & 0xFFFFu) - 1;
+                    const uint32_t q1 = qq - ((uint32_t)(__shfl_sync(FULL, exc, hb | wsel) >> sh) & 0x1FFFFFu);
+                    // row i inside the word: lane hl holds rows 2hl, 2hl+1; scan of the pairs
+                    const int lw = 32 * wsel + 2 * hl;
+                    const uint32_t lv0 = lw < r ? (uint32_t)getf(s.lc[lw], X) : 0u;
+                    const uint32_t lv1 = lw + 1 < r ? (uint32_t)getf(s.lc[lw + 1], X) : 0u;
+                    uint32_t inc2 = lv0 + lv1;
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(FULL, inc2, o);
-                        if (lane >= o) inc2 += t;
+                    for (int o = 1; o < 16; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(FULL, inc2, o, 16);
+                        if (hl >= o) inc2 += t;
                     }
-                    const int L = __ffs(__ballot_sync(FULL, inc2 > q1)) - 1;
-                    const int i = 32 * wsel + L;
+                    const uint32_t ex2 = inc2 - lv0 - lv1;            // later counts before row 2hl
+                    const int Lp = __ffs((__ballot_sync(FULL, inc2 > q1) >> hb) & 0xFFFFu) - 1;
+                    const uint32_t exL = __shfl_sync(FULL, ex2, hb | Lp), l0L = __shfl_sync(FULL, lv0, hb | Lp);
+                    const int second = exL + l0L <= q1 ? 1 : 0;         // row 2Lp+1 (else 2Lp)
+                    const int i = 32 * wsel + 2 * Lp + second;
+                    const uint32_t acc = exL + (second ? l0L : 0u);
                     // j: the (q1 - acc)-th later member of row i's X class
                     const uint16_t *nxX = s.nxh + X * RM;
                     int j = i;
 #pragma unroll 1
-                    for (uint32_t hops = q1 - __shfl_sync(FULL, inc2 - lv, L) + 1; hops; --hops) j = nxX[j];
+                    for (uint32_t hops = q1 - acc + 1; hops; --hops) j = nxX[j];
                     const int al = d ? j : i, be = d ? i : j;
                     // (Y,Z) = (V,W) / (W,U) / (U,V) for X = U / V / W, swapped if e
                     const unsigned yz = (0x148269u >> (4 * (2 * X + e))) & 15u;
                     const int Y = yz & 3, Z = yz >> 2;
                     const uint32_t sga = s.wsg(al), sgb = s.wsg(be);
                     const bool sneg = P::RING == FG_ZT && X == 2 && sga != sgb;
-                    bool v = true;
+                    bool v = a2 < kf;
                     const F ya = s.key(Y, al), yb = s.key(Y, be), za = s.key(Z, al), zb = s.key(Z, be);
                     // the actual w carries its sign bit (stored up to sign)
                     const F yaF = P::sel(Y == 2 && sga, P::neg(ya), ya);
@@ -663,13 +676,20 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     const F zbF = P::sel(Z == 2 && sgb, P::neg(zb), zb);
                     const F ny = P::add(yaF, P::sel(sneg, P::neg(ybF), ybF), v);   // y_a + s y_b
                     const F nz = P::sub(zbF, zaF, v);                              // z_b - z_a
-                    if (!v) continue;
-                    alpha = al;
-                    beta = be;
-                    fY = Y;
-                    fZ = Z;
-                    fny = ny;
-                    fnz = nz;
+                    const uint32_t vb = __ballot_sync(FULL, v);
+                    if (!vb) {
+                        draws += (at + 1 < kf) ? 2 : 1;
+                        continue;
+                    }
+                    const int win = (vb & 0xFFFFu) ? 0 : 1;             // the earlier valid draw
+                    const int src = win << 4;
+                    draws += (int)win + 1;
+                    alpha = __shfl_sync(FULL, al, src);
+                    beta = __shfl_sync(FULL, be, src);
+                    fY = __shfl_sync(FULL, Y, src);
+                    fZ = __shfl_sync(FULL, Z, src);
+                    fny = P::shfl(ny, src);
+                    fnz = P::shfl(nz, src);
                     ok = true;
                     break;
                 }
