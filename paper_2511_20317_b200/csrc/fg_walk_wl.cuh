@@ -34,6 +34,9 @@ using namespace fgd;
 
 constexpr int NIL = 1023;
 constexpr int PXS = 9;                         // Philox table stride (32 steps x 9 words)
+#ifndef WL_DRAWS
+#define WL_DRAWS 4                             // flip draws evaluated at once (lane groups of 32 / WL_DRAWS): 4 measured best (2: -1..-13 %, 8: -3..-13 %)
+#endif
 constexpr int IMG_SCALARS = 8;                 // nCU, nCV, nCW, dset lo, dset hi, nD, dover, r
 
 // class image per walker (HBM): nxh (3 RM u16), lc (RM), tw (32), wsb (16), scalars
@@ -593,30 +596,43 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             int fY = 0, fZ = 0;
             F fny = P::make(0, 0), fnz = fny;
 
-            // ---- R11 try_flip: draws over 4|C| (R9), two at a time: half h of the warp
-            // (16 lanes) evaluates draw 2t + h; the first valid one in draw order is the one
-            // the sequential loop commits (draws are addressed, not consumed) ----
+            // ---- R11 try_flip: draws over 4|C| (R9), ND at a time: lane group g (GL lanes)
+            // evaluates draw ND*t + g; the first valid one in draw order is the one the
+            // sequential loop commits (draws are addressed, not consumed) ----
             if (nC) {
-                const int h = lane >> 4, hl = lane & 15, hb = lane & 16;
+                constexpr int ND = WL_DRAWS, GL = 32 / ND;
+                constexpr int WPL = (16 + GL - 1) / GL;           // prefix words per lane (nwd <= 16)
+                constexpr int RPL = 32 / GL;                       // rows of the word per lane
+                const unsigned gmask = GL == 32 ? FULL : ((1u << GL) - 1u);
+                const int grp = lane / GL, gl = lane % GL, gb = grp * GL;
                 // prefix of the word totals, once per step (the list is not rebuilt between
-                // draws): lane hl of each half holds the inclusive sums of words 0..hl,
-                // 3 x 21-bit fields
-                uint64_t tv = 0;
-                if (hl < nwd) {
-                    const uint32_t t0 = s.tw[hl], t1 = s.tw[16 + hl];
-                    tv = (uint64_t)(t0 & 0xFFFFu) | ((uint64_t)(t0 >> 16) << 21) | ((uint64_t)t1 << 42);
-                }
-                uint64_t inc = tv;
+                // draws), 3 x 21-bit fields: lane gl of each group holds words WPL*gl ...
+                uint64_t winc[WPL];
+                uint64_t lsum = 0;
 #pragma unroll
-                for (int o = 1; o < 16; o <<= 1) {
-                    const uint64_t t = __shfl_up_sync(FULL, inc, o, 16);
-                    if (hl >= o) inc += t;
+                for (int q = 0; q < WPL; ++q) {
+                    const int w = WPL * gl + q;
+                    uint64_t tv = 0;
+                    if (w < nwd) {
+                        const uint32_t t0 = s.tw[w], t1 = s.tw[16 + w];
+                        tv = (uint64_t)(t0 & 0xFFFFu) | ((uint64_t)(t0 >> 16) << 21) | ((uint64_t)t1 << 42);
+                    }
+                    lsum += tv;
+                    winc[q] = lsum;                                // within-lane inclusive
                 }
-                const uint64_t exc = inc - tv;
+                uint64_t linc = lsum;
+#pragma unroll
+                for (int o = 1; o < GL; o <<= 1) {
+                    const uint64_t t = __shfl_up_sync(FULL, linc, o, GL);
+                    if (gl >= o) linc += t;
+                }
+                const uint64_t lexc = linc - lsum;                  // words before WPL*gl
+#pragma unroll
+                for (int q = 0; q < WPL; ++q) winc[q] += lexc;
                 uint32_t e0 = 0, e1 = 0, e2 = 0, e3 = 0, cb = 0xFFFFFFFFu;
 #pragma unroll 1
-                for (uint32_t at = 0; at < kf; at += 2) {
-                    const uint32_t a2 = at + (uint32_t)h;               // this half's draw
+                for (uint32_t at = 0; at < kf; at += ND) {
+                    const uint32_t a2 = at + (uint32_t)grp;             // this group's draw
                     uint32_t x;
                     if (a2 == 0) x = pw[0];
                     else if (a2 <= 4) x = pw[3 + a2];
@@ -635,27 +651,55 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     const uint32_t g1 = idx >= nU, g2 = idx >= nU + nV;
                     const int X = (int)(g1 + g2);
                     const uint32_t qq = idx - (g1 ? nU : 0u) - (g2 ? nV : 0u);
-                    // the word holding row i
+                    // the word holding row i: the first word whose inclusive prefix exceeds qq
                     const int sh = 21 * X;
-                    const uint32_t wb = __ballot_sync(FULL, hl < nwd && ((uint32_t)(inc >> sh) & 0x1FFFFFu) > qq);
-                    const int wsel = __ffs((wb >> hb) & 0xFFFFu) - 1;
-                    const uint32_t q1 = qq - ((uint32_t)(__shfl_sync(FULL, exc, hb | wsel) >> sh) & 0x1FFFFFu);
-                    // row i inside the word: lane hl holds rows 2hl, 2hl+1; scan of the pairs
-                    const int lw = 32 * wsel + 2 * hl;
-                    const uint32_t lv0 = lw < r ? (uint32_t)getf(s.lc[lw], X) : 0u;
-                    const uint32_t lv1 = lw + 1 < r ? (uint32_t)getf(s.lc[lw + 1], X) : 0u;
-                    uint32_t inc2 = lv0 + lv1;
+                    int qf = WPL;
 #pragma unroll
-                    for (int o = 1; o < 16; o <<= 1) {
-                        const uint32_t t = __shfl_up_sync(FULL, inc2, o, 16);
-                        if (hl >= o) inc2 += t;
+                    for (int q = WPL - 1; q >= 0; --q)
+                        if (WPL * gl + q < nwd && ((uint32_t)(winc[q] >> sh) & 0x1FFFFFu) > qq) qf = q;
+                    const int Lw = __ffs((__ballot_sync(FULL, qf < WPL) >> gb) & gmask) - 1;
+                    const int qsel = __shfl_sync(FULL, qf, gb | Lw);
+                    const int wsel = WPL * Lw + qsel;
+                    // prefix before word wsel: lane Lw's inclusive sum of its words before qsel
+                    uint64_t wexc = lexc;
+#pragma unroll
+                    for (int q = 0; q < WPL; ++q)
+                        if (q < qf && q < WPL) wexc = winc[q];
+                    wexc = __shfl_sync(FULL, qsel == 0 ? lexc : wexc, gb | Lw);
+                    // (lane Lw: qf == qsel, so wexc is the inclusive sum of word qsel-1)
+                    const uint32_t q1 = qq - ((uint32_t)(wexc >> sh) & 0x1FFFFFu);
+                    // row i inside the word: lane gl holds rows RPL*gl ... of word wsel
+                    uint32_t lv[RPL];
+                    uint32_t rsum = 0;
+#pragma unroll
+                    for (int q = 0; q < RPL; ++q) {
+                        const int lw = 32 * wsel + RPL * gl + q;
+                        lv[q] = lw < r ? (uint32_t)getf(s.lc[lw], X) : 0u;
+                        rsum += lv[q];
                     }
-                    const uint32_t ex2 = inc2 - lv0 - lv1;            // later counts before row 2hl
-                    const int Lp = __ffs((__ballot_sync(FULL, inc2 > q1) >> hb) & 0xFFFFu) - 1;
-                    const uint32_t exL = __shfl_sync(FULL, ex2, hb | Lp), l0L = __shfl_sync(FULL, lv0, hb | Lp);
-                    const int second = exL + l0L <= q1 ? 1 : 0;         // row 2Lp+1 (else 2Lp)
-                    const int i = 32 * wsel + 2 * Lp + second;
-                    const uint32_t acc = exL + (second ? l0L : 0u);
+                    uint32_t rinc = rsum;
+#pragma unroll
+                    for (int o = 1; o < GL; o <<= 1) {
+                        const uint32_t t = __shfl_up_sync(FULL, rinc, o, GL);
+                        if (gl >= o) rinc += t;
+                    }
+                    const uint32_t rexc = rinc - rsum;                  // later counts before row RPL*gl
+                    const int Lr = __ffs((__ballot_sync(FULL, rinc > q1) >> gb) & gmask) - 1;
+                    // within lane Lr's rows: the first row whose running sum exceeds q1
+                    uint32_t run = rexc;
+                    int qr = RPL - 1;
+                    uint32_t accr = rexc;
+#pragma unroll
+                    for (int q = RPL - 1; q >= 0; --q) {
+                        uint32_t before = rexc;
+#pragma unroll
+                        for (int q2 = 0; q2 < q; ++q2) before += lv[q2];
+                        if (before + lv[q] > q1) { qr = q; accr = before; }
+                    }
+                    (void)run;
+                    const int rq = __shfl_sync(FULL, qr, gb | Lr);
+                    const uint32_t acc = __shfl_sync(FULL, accr, gb | Lr);
+                    const int i = 32 * wsel + RPL * Lr + rq;
                     // j: the (q1 - acc)-th later member of row i's X class
                     const uint16_t *nxX = s.nxh + X * RM;
                     int j = i;
@@ -678,12 +722,12 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     const F nz = P::sub(zbF, zaF, v);                              // z_b - z_a
                     const uint32_t vb = __ballot_sync(FULL, v);
                     if (!vb) {
-                        draws += (at + 1 < kf) ? 2 : 1;
+                        draws += (kf - at) < (uint32_t)ND ? (int)(kf - at) : ND;
                         continue;
                     }
-                    const int win = (vb & 0xFFFFu) ? 0 : 1;             // the earlier valid draw
-                    const int src = win << 4;
-                    draws += (int)win + 1;
+                    const int win = (__ffs(vb) - 1) / GL;              // the earliest valid draw
+                    const int src = win * GL;
+                    draws += win + 1;
                     alpha = __shfl_sync(FULL, al, src);
                     beta = __shfl_sync(FULL, be, src);
                     fY = __shfl_sync(FULL, Y, src);
