@@ -13,7 +13,7 @@
 namespace {
 
 constexpr uint32_t REC_MAGIC = 0x46475231u;   // "FGR1"
-constexpr uint32_t STATE_MAGIC = 0x46475332u; // "FGS2": planes packed to the factor width
+constexpr uint32_t STATE_MAGIC = 0x46475333u; // "FGS3": packed planes; walk_wl word totals as 3 x 21-bit fields
 
 struct RecHdr {          // 64 bytes, followed by 6*r_cap u64 planes
     uint32_t magic;

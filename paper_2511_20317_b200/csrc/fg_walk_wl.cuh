@@ -13,7 +13,8 @@
 //   wsb        the signs of the w factors, one bit per row (the stored W key is the
 //              positive form, W classes are "equal up to sign")
 //   lc[l]      later counts of the three classes, 10 bits each (R10)
-//   tw[w]      per 32-row word the sum of its rows' later counts (U | V << 16; W)
+//   tw[w]      per 32-row word the sum of its rows' later counts, 3 x 21-bit fields of a u64
+//              (U | V << 21 | W << 42: the draw's prefix scan adds them as they are)
 // so a draw (R11) is a lookup in the per-step prefix of the word totals, one warp scan
 // of the word's later counts and `hops` next-pointer steps, and a flip commit is ONE
 // compare pass over the rows
@@ -64,7 +65,7 @@ template <class P> struct WS {
     uint16_t *nxh;        // [3][RM]
     uint32_t *lc;         // [RM]
     uint32_t *wsb;        // [16]
-    uint32_t *tw;         // [32]: U | V << 16 at w, W at 16 + w
+    uint32_t *tw;         // [32] = 16 u64: U | V << 21 | W << 42 per word
     int nwd, RM;
     __device__ __forceinline__ typename P::F key(int X, int l) const { return fac[X * RM + l]; }
     __device__ __forceinline__ int nxt(int X, int l) const { return (int)nxh[X * RM + l]; }
@@ -90,8 +91,8 @@ template <class P> struct WS {
     // word total of role X (lane 0 only)
     __device__ __forceinline__ void tw_add(int w, int X, int d) const
     {
-        if (X == 2) tw[16 + w] += (uint32_t)d;
-        else tw[w] += (uint32_t)d << (16 * X);
+        // (a negative d wraps modulo 2^64 and subtracts from its field only: fields stay >= 0)
+        reinterpret_cast<unsigned long long *>(tw)[w] += (unsigned long long)(long long)d << (21 * X);
     }
 };
 
@@ -228,7 +229,7 @@ __device__ __noinline__ uint32_t check_structure(WS<P> s, int r, uint32_t nCU, u
                 if (s.nxt(X, l) != first) bad |= 2u;
             }
             const int sum = __reduce_add_sync(FULL, (uint32_t)cnt);
-            const uint32_t t = X == 2 ? s.tw[16 + w] : ((s.tw[w] >> (16 * X)) & 0xFFFFu);
+            const uint32_t t = (uint32_t)(reinterpret_cast<const unsigned long long *>(s.tw)[w] >> (21 * X)) & 0x1FFFFFu;
             if ((uint32_t)sum != t) bad |= 4u;
             tot[X] += (uint32_t)sum;
         }
@@ -614,8 +615,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     const int w = WPL * gl + q;
                     uint64_t tv = 0;
                     if (w < nwd) {
-                        const uint32_t t0 = s.tw[w], t1 = s.tw[16 + w];
-                        tv = (uint64_t)(t0 & 0xFFFFu) | ((uint64_t)(t0 >> 16) << 21) | ((uint64_t)t1 << 42);
+                        tv = reinterpret_cast<const unsigned long long *>(s.tw)[w];
                     }
                     lsum += tv;
                     winc[q] = lsum;                                // within-lane inclusive
