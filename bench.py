@@ -55,10 +55,10 @@ NCU_TRAFFIC = {
     ("walk_q4<PZ2>", "c2_333_z2"): (28.701952e6 + 36.486656e6, "profiles/r02_ncu_walk_q4_c2_333_z2.txt", 49.32, 40.6),
     ("walk_ql<P16>", "c3_444_zt"): (76.071424e6 + 60.55424e6, "profiles/r02_ncu_walk_ql_c3_444_zt.txt", 51.59, 51.0),
     ("walk_ql<PZ2>", "c3_444_z2"): (49.316096e6 + 51.712768e6, "profiles/r02_ncu_walk_ql_c3_444_z2.txt", 53.40, 53.5),
-    ("walk_wl<P32>", "c4_555_zt"): (180.839424e6 + 137.13792e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 74.14, 73.9),
-    ("walk_wl<P64>", "c5_4512_zt"): (203.371008e6 + 97.247488e6, "profiles/r02_ncu_walk_wl_c5_4512_zt.txt", 56.50, 64.8),
-    ("walk_wl<P64>", "c5_5610_zt"): (245.697536e6 + 134.351872e6, "profiles/r02_ncu_walk_wl_c5_5610_zt.txt", 53.15, 65.5),
-    ("walk_wl<P64>", "c5_679_zt"): (310.248192e6 + 185.97376e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 43.96, 55.7),
+    ("walk_wl<P32>", "c4_555_zt"): (180.3584e6 + 138.653952e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 74.21, 74.8),
+    ("walk_wl<P64>", "c5_4512_zt"): (202.623488e6 + 96.183552e6, "profiles/r02_ncu_walk_wl_c5_4512_zt.txt", 56.96, 65.6),
+    ("walk_wl<P64>", "c5_5610_zt"): (245.70112e6 + 132.997376e6, "profiles/r02_ncu_walk_wl_c5_5610_zt.txt", 53.49, 66.2),
+    ("walk_wl<P64>", "c5_679_zt"): (308.619776e6 + 185.382144e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 44.40, 56.5),
 }
 
 
