@@ -34,7 +34,9 @@ namespace fgwl {
 using namespace fgd;
 
 constexpr int NIL = 1023;
-constexpr int PXS = 9;                         // Philox table stride (32 steps x 9 words)
+constexpr int PXT = 16, PXS = 6;               // Philox table: 16 steps x 6 words (draw 0, Bernoulli
+                                               // flags, block 2 = draws 1-4): 384 B, so (6,7,9) walkers fit
+                                               // 9 per SM (8 with a 32-step table)
 #ifndef WL_DRAWS
 #define WL_DRAWS 4                             // flip draws evaluated at once (lane groups of 32 / WL_DRAWS): 4 measured best (2: -1..-13 %, 8: -3..-13 %)
 #endif
@@ -249,8 +251,8 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
     s.lc = reinterpret_cast<uint32_t *>(s.fac + 3 * RM);
     s.tw = s.lc + RM;
     s.wsb = s.tw + 32;
-    uint32_t *px = s.wsb + 16;                                 // Philox table [32][PXS]
-    uint32_t *rc = px + 32 * PXS;                              // 8 rare counters
+    uint32_t *px = s.wsb + 16;                                 // Philox table [PXT][PXS]
+    uint32_t *rc = px + PXT * PXS;                             // 8 rare counters
     s.nxh = reinterpret_cast<uint16_t *>(rc + 8);
     s.nwd = nwd;
     s.RM = RM;
@@ -570,20 +572,24 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             return (int)__reduce_add_sync(FULL, (uint32_t)v);
         };
 
-        int boff = 32;
+        int boff = PXT;
         const uint32_t nsteps = (uint32_t)a.steps;
 #pragma unroll 1
         for (uint32_t it = 0; it < nsteps; ++it, ++step, ++boff) {
-            if (boff == 32) {
-                // Philox (R8) blocks 0 and 2 of the next 32 steps, lane-parallel
+            if (boff == PXT) {
+                // Philox (R8) of the next 16 steps, one block per lane: lane L < 16 block 0 of
+                // step + L (draw 0 + the Bernoulli words), lane 16 + L block 2 (draws 1-4)
                 uint32_t o0, o1, o2, o3;
-                philox_block(seed, step + lane, wid, 0u, o0, o1, o2, o3);
-                px[lane * PXS + 0] = o0;
-                px[lane * PXS + 1] = (o1 < a.thr_eq ? 1u : 0u) | (o2 < a.thr_reduce ? 2u : 0u) |
-                                     (o3 < a.thr_expand ? 4u : 0u);
-                philox_block(seed, step + lane, wid, 2u, o0, o1, o2, o3);
-                px[lane * PXS + 4] = o0; px[lane * PXS + 5] = o1;
-                px[lane * PXS + 6] = o2; px[lane * PXS + 7] = o3;
+                const int L = lane & 15;
+                philox_block(seed, step + L, wid, lane < 16 ? 0u : 2u, o0, o1, o2, o3);
+                if (lane < 16) {
+                    px[L * PXS + 0] = o0;
+                    px[L * PXS + 1] = (o1 < a.thr_eq ? 1u : 0u) | (o2 < a.thr_reduce ? 2u : 0u) |
+                                      (o3 < a.thr_expand ? 4u : 0u);
+                } else {
+                    px[L * PXS + 2] = o0; px[L * PXS + 3] = o1;
+                    px[L * PXS + 4] = o2; px[L * PXS + 5] = o3;
+                }
                 __syncwarp();
                 boff = 0;
             }
@@ -635,7 +641,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     const uint32_t a2 = at + (uint32_t)grp;             // this group's draw
                     uint32_t x;
                     if (a2 == 0) x = pw[0];
-                    else if (a2 <= 4) x = pw[3 + a2];
+                    else if (a2 <= 4) x = pw[1 + a2];
                     else {
                         const uint32_t slot = 7 + a2, blk = slot >> 2;
                         if (blk != cb) {
@@ -954,7 +960,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
 // counters, next arrays (3 x RM u16)
 template <class P> size_t wl_smem(int nwd)
 {
-    return (size_t)3 * 32 * nwd * sizeof(typename P::F) + 32 * nwd * 4 + 32 * 4 + 16 * 4 + 32 * PXS * 4 + 8 * 4 +
+    return (size_t)3 * 32 * nwd * sizeof(typename P::F) + 32 * nwd * 4 + 32 * 4 + 16 * 4 + PXT * PXS * 4 + 8 * 4 +
            3 * 32 * nwd * 2;
 }
 
