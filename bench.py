@@ -56,9 +56,9 @@ NCU_TRAFFIC = {
     ("walk_ql<P16>", "c3_444_zt"): (76.071424e6 + 60.55424e6, "profiles/r02_ncu_walk_ql_c3_444_zt.txt", 51.59, 51.0),
     ("walk_ql<PZ2>", "c3_444_z2"): (49.316096e6 + 51.712768e6, "profiles/r02_ncu_walk_ql_c3_444_z2.txt", 53.40, 53.5),
     ("walk_wl<P32>", "c4_555_zt"): (180.3584e6 + 138.653952e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 74.21, 74.8),
-    ("walk_wl<P64>", "c5_4512_zt"): (202.623488e6 + 96.183552e6, "profiles/r02_ncu_walk_wl_c5_4512_zt.txt", 56.96, 65.6),
+    ("walk_wl<P64>", "c5_4512_zt"): (203.328512e6 + 96.339968e6, "profiles/r02_ncu_walk_wl_c5_4512_zt.txt", 58.76, 68.2),
     ("walk_wl<P64>", "c5_5610_zt"): (245.70112e6 + 132.997376e6, "profiles/r02_ncu_walk_wl_c5_5610_zt.txt", 53.49, 66.2),
-    ("walk_wl<P64>", "c5_679_zt"): (308.619776e6 + 185.382144e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 44.40, 56.5),
+    ("walk_wl<P64>", "c5_679_zt"): (310.861312e6 + 186.3488e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 48.24, 60.1),
 }
 
 
