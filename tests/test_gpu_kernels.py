@@ -256,3 +256,29 @@ def test_q4_chunked_tasks(fg, orc, case):
     _check(got, ref, None)
     assert np.all(got["step"] == steps)
     assert g.stats()["verify_fail"] == 0
+
+
+def test_q4_chunked_complexity_mode(fg, orc):
+    """R24 (naive-complexity mode) through walk_q4's chunked tasks (FG_Q4_CHUNKS=6):
+    every walker bit-exact, the best-by-additions image handed over between chunks."""
+    m, n, p, R, W, steps, seed = 3, 3, 3, 32, 203, 1800, 0xCAFE
+    w = orc.walker(m, n, p, ZT, R, walker_id=3)
+    w.seed_naive()
+    w.walk(5000, 77)
+    start = w.rows(0)
+    old = os.environ.get("FG_Q4_CHUNKS")
+    os.environ["FG_Q4_CHUNKS"] = "6"
+    try:
+        g = _ctx(fg, "q4", m, n, p, ZT, R, W)
+        g.seed_pool(start)
+        g.walk(steps, seed, fg.params_default(flags=fg.FG_FLAG_COMPLEXITY))
+    finally:
+        if old is None:
+            del os.environ["FG_Q4_CHUNKS"]
+        else:
+            os.environ["FG_Q4_CHUNKS"] = old
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ZT, R, W, 0, steps, seed, seed_coeffs=start,
+                          params=OracleParams.default(mode=1))
+    _check(got, ref, None)
+    assert np.all(got["r"] == start.shape[0])
