@@ -4,5 +4,4 @@ cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -x -q ${TESTS_K:+-k "$TESTS_K"} > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests.log
-if [ -n "$ALSO_H16" ]; then FG_WALK_KERNEL=h16 timeout 900 python -m pytest tests -m gpu -x -q -k "c1 or c2 or edge or split" > gpurun_out/gpu_tests_h16.log 2>&1; echo "tests rc=$?" >> gpurun_out/gpu_tests_h16.log; fi
 timeout 600 python bench.py ${BENCH_ARGS:---steps 10 --warmup 3 --cpu-seconds 8} > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
