@@ -982,20 +982,35 @@ cudaError_t launch_wl_m(const WalkArgs &a, int num_sms, cudaStream_t st)
     return cudaGetLastError();
 }
 
-// register budget (resident warps per SM the compiler must allow): FG_WL_MINB selects
-// an instantiation for A/B timing
+// register budget (resident warps per SM the compiler must allow).  Measured
+// (scripts/gpu_r02_minb2.sh, gpu_r02_minb3.sh, profiles/r02_ab_wl_minb.txt): P32 (C4, register
+// limited) runs best with 18 warps' worth (113 registers; 96 spills more, 128 loses warps);
+// the 16-byte layouts are shared-memory limited, so the budget follows the warps that fit:
+// 14 for (4,5,12) (14 fit), 11 for (5,6,10) and (6,7,9) (11 / 9 fit): +2 ... +5 % over 128
+// registers.  FG_WL_MINB overrides (A/B).
 template <class P>
 cudaError_t launch_wl(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     const char *ev = getenv("FG_WL_MINB");
-    const int mb = ev ? atoi(ev) : 0;
-    if (mb == 1) return launch_wl_m<P, 1>(a, num_sms, st);
+    int mb = ev ? atoi(ev) : 0;
+    if (mb == 0) {
+        if (std::is_same<P, P32>::value) {
+            mb = 18;
+        } else if (sizeof(typename P::F) > 8) {
+            int dev = 0, per_sm = 0, reserve = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+            cudaDeviceGetAttribute(&reserve, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+            const int fit = per_sm / (int)(wl_smem<P>((a.R + 31) / 32) + reserve);
+            mb = fit >= 16 ? 16 : (fit >= 14 ? 14 : 11);
+        } else {
+            mb = 16;
+        }
+    }
+    if (mb == 11) return launch_wl_m<P, 11>(a, num_sms, st);
+    if (mb == 14) return launch_wl_m<P, 14>(a, num_sms, st);
+    if (mb == 18) return launch_wl_m<P, 18>(a, num_sms, st);
     if (mb == 20) return launch_wl_m<P, 20>(a, num_sms, st);
-    if (mb == 24) return launch_wl_m<P, 24>(a, num_sms, st);
-    if (mb == 16) return launch_wl_m<P, 16>(a, num_sms, st);
-    // measured (scripts/gpu_r02_minb.sh): P32 (C4) runs best with 20 resident warps' worth
-    // of registers (96), the P64 layouts with 16 (128 registers; 96 spills too much)
-    if (std::is_same<P, P32>::value) return launch_wl_m<P, 20>(a, num_sms, st);
     return launch_wl_m<P, 16>(a, num_sms, st);
 }
 
