@@ -32,6 +32,7 @@
 //
 // Same readings, draw order and digest as fg_walk.cu / the oracle; parity:
 // tests/test_gpu_parity.py, tests/test_gpu_kernels.py, tests/test_gpu_fuzz.py.
+#include <cstdio>
 #include <cstdlib>
 #include <type_traits>
 #include "fg_device.cuh"
@@ -40,8 +41,12 @@ using namespace fgd;
 
 #define Q4_THREADS 32
 #define Q4_WARPS (Q4_THREADS / 32)
-#ifndef Q4_MINB
-#define Q4_MINB 14             // 146 registers: no spills; 14 warps x 148 SMs >= the C2 population (2048 warps)
+// 128 registers = 4 warps per SMSP (the register file is split per SMSP), 16 per SM; a
+// __maxnreg__ cap measured +4 % on C2 over __launch_bounds__(32, 14/16), which ptxas also
+// compiled to 128 registers but with spills in the Z_2 / R24 instantiations
+// (profiles/r02_ab_q4_chunks.txt)
+#ifndef Q4_MAXNREG
+#define Q4_MAXNREG 128
 #endif
 #ifndef Q4_ORDER
 #define Q4_ORDER 0             // chunked tasks: 0 = completion order (ready queue), 1 = chunk-major
@@ -63,7 +68,7 @@ __device__ __forceinline__ int nth_bit_q4(uint32_t x, uint32_t t)
 }
 
 template <class P, bool CM>
-__global__ void __launch_bounds__(Q4_THREADS, Q4_MINB) walk_q4(WalkArgs a)
+__global__ void __maxnreg__(Q4_MAXNREG) walk_q4(WalkArgs a)
 {
     typedef typename P::F F;
     static_assert(sizeof(F) == 4, "one-word factor layouts only");
@@ -867,6 +872,15 @@ template <class P, bool CM>
 cudaError_t launch_q4_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     const int64_t groups = (a.num_walkers + 7) / 8;
+    // all of the unified L1 as shared memory: 1-warp CTAs with 11 KB of static shared memory
+    // each would otherwise be capped by the driver's default carveout, not by registers
+    static bool carve = false;
+    if (!carve) {
+        cudaError_t ce = cudaFuncSetAttribute(walk_q4<P, CM>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                              (int)cudaSharedmemCarveoutMaxShared);
+        if (ce != cudaSuccess) return ce;
+        carve = true;
+    }
     int bps = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_q4<P, CM>, Q4_THREADS, 0);
     if (e != cudaSuccess) return e;
@@ -891,6 +905,9 @@ cudaError_t launch_q4_m(const WalkArgs &a, int num_sms, cudaStream_t st)
     } else {
         blocks = (groups + Q4_WARPS - 1) / Q4_WARPS;
     }
+    if (getenv("FG_DBG_LAUNCH"))
+        fprintf(stderr, "walk_q4: %d CTAs/SM, resident %lld warps, groups %lld, chunks %u, grid %lld\n", bps,
+                (long long)resident, (long long)groups, b.chunks, (long long)blocks);
     walk_q4<P, CM><<<(unsigned)blocks, Q4_THREADS, 0, st>>>(b);
     return cudaGetLastError();
 }
