@@ -51,8 +51,8 @@ def parse():
 # (kernel, workload) -> (dram bytes per launch, profile it comes from)
 # and the capture's issue / ALU-pipe utilisation (the north star's "% int-issue" figures)
 NCU_TRAFFIC = {
-    ("walk_q4<P16>", "c2_333_zt"): (54.125312e6 + 27.88352e6, "profiles/r02_ncu_walk_q4_c2_333_zt.txt", 55.66, 50.2),
-    ("walk_q4<PZ2>", "c2_333_z2"): (28.701952e6 + 36.486656e6, "profiles/r02_ncu_walk_q4_c2_333_z2.txt", 49.32, 40.6),
+    ("walk_q4<P16>", "c2_333_zt"): (54.130432e6 + 30.0288e6, "profiles/r02_ncu_walk_q4_c2_333_zt.txt", 58.37, 52.1),
+    ("walk_q4<PZ2>", "c2_333_z2"): (28.580608e6 + 34.312704e6, "profiles/r02_ncu_walk_q4_c2_333_z2.txt", 52.10, 42.2),
     ("walk_ql<P16>", "c3_444_zt"): (76.071424e6 + 60.55424e6, "profiles/r02_ncu_walk_ql_c3_444_zt.txt", 51.59, 51.0),
     ("walk_ql<PZ2>", "c3_444_z2"): (49.316096e6 + 51.712768e6, "profiles/r02_ncu_walk_ql_c3_444_z2.txt", 53.40, 53.5),
     ("walk_wl<P32>", "c4_555_zt"): (180.3584e6 + 138.653952e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 74.21, 74.8),
