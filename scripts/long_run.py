@@ -4,7 +4,8 @@ phases from naive seeds (no restarts, no Resize); the ladder is exact (verified 
 improvements' step indices, fg_rank_first_steps), the best scheme is re-verified on the
 host (fg_verify, exact integer Brent check) and written with its invariants.
 
-  python scripts/long_run.py <workload> <seconds> <out.json> [restart_every_phases slack]
+  python scripts/long_run.py <workload | m,n,p,ring,R,walkers[,target]> <seconds> <out.json>
+                             [restart_every_phases slack]
 
 With a restart period, every that many phases the box-wide best becomes the pool
 (fg_export_best -> fg_import_best) and walkers whose best rank exceeds it by more than
@@ -30,7 +31,14 @@ def main():
     every = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     slack = int(sys.argv[5]) if len(sys.argv) > 5 else 2
     restarted = 0
-    wl = WORKLOADS[key]
+    if key in WORKLOADS:
+        wl = WORKLOADS[key]
+    else:
+        # an ad-hoc format "m,n,p,ring,R,walkers[,target]" (PAPER tables' formats)
+        from paper_2511_20317_b200.inputs import Workload
+        f = [int(x) for x in key.split(",")]
+        wl = Workload(f"({f[0]},{f[1]},{f[2]}) {'Z_T' if f[3] == 0 else 'Z_2'} naive {f[0] * f[1] * f[2]}",
+                      f[0], f[1], f[2], f[3], f[4], f[5], f[6] if len(f) > 6 else None, 99)
     S = 10000 if wl.r_cap <= 32 else PHASE_MULTI
     stream = torch.cuda.current_stream()
     g = fg.FlipGraph(wl.m, wl.n, wl.p, wl.ring, wl.r_cap, wl.walkers, 0, 0, stream.cuda_stream)
