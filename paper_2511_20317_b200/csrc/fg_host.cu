@@ -614,9 +614,10 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     a.ring = c->d_ring;
     a.ring_tail = &c->d_misc->ring_tail;
     a.wl_img = c->d_wl_img;
-    // the complexity mode (R24) runs the round-1 kernels; walk_wl's layouts map to walk_wm
+    // the complexity mode (R24): walk_wl / walk_wm pick their CM instance from a.mode,
+    // walk_ql contexts run it on walk_wl, walk_q4 / walk_w32 on their CM instance
     int kind = c->kind;
-    if (a.mode) kind = fg_kind_is_wl(kind) ? fg_multi_kind(c->ring, c->maxlen, c->R) : fg_kind_for_mode(kind);
+    if (a.mode && !fg_kind_is_wl(kind)) kind = fg_kind_for_mode(kind);
     a.dbg = getenv("FG_DBG") ? (uint32_t)strtoul(getenv("FG_DBG"), nullptr, 0) : 0u;
     a.dbgbuf = c->d_misc->dbgbuf;
     VerifyArgs v;
@@ -640,7 +641,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
         CK(cudaEventRecord(c->ev0, c->stream));
         a.img_valid = c->img_valid ? 1u : 0u;
         CK(fg_launch_walk(kind, a, c->num_sms, c->stream));
-        c->img_valid = fg_kind_is_wl(kind);
+        c->img_valid = fg_kind_is_wl(kind) && a.wl_img != nullptr;   // R24 on walk_ql contexts: no image
         CK(cudaEventRecord(c->ev1, c->stream));
         CK(fg_launch_verify(v, c->stream));
         CK(cudaEventRecord(c->ev2, c->stream));

@@ -615,8 +615,8 @@ int fg_pick_kernel(int ring, int maxlen, int R)
 int fg_kind_for_mode(int kind)
 {
     switch (kind) {
-    case FG_K_QL_P16: return FG_K_WM_P16;
-    case FG_K_QL_Z2: return FG_K_WM_Z2;
+    case FG_K_QL_P16: return FG_K_WL_P16;
+    case FG_K_QL_Z2: return FG_K_WL_Z2;
     default: return kind;
     }
 }

@@ -51,6 +51,9 @@ using namespace fgd;
 #ifndef Q4_ORDER
 #define Q4_ORDER 0             // chunked tasks: 0 = completion order (ready queue), 1 = chunk-major
 #endif
+#ifndef Q4_SPIN_MAX
+#define Q4_SPIN_MAX 256        // a warp waiting for its next chunk sleeps 256 ns, doubling up to this
+#endif
 
 namespace {
 
@@ -106,10 +109,14 @@ __global__ void __maxnreg__(Q4_MAXNREG) walk_q4(WalkArgs a)
                     // chunk-major: chunk k / n_groups of group k % n_groups, after its predecessor
                     g1 = (uint32_t)(k % (unsigned long long)n_groups) + 1u;
                     ch = (uint32_t)(k / (unsigned long long)n_groups);
-                    while (*(volatile uint32_t *)(a.task_done + (g1 - 1u)) < ch) __nanosleep(256);
+                    for (uint32_t ns = 256; *(volatile uint32_t *)(a.task_done + (g1 - 1u)) < ch;
+                         ns = ns < Q4_SPIN_MAX ? 2 * ns : ns)
+                        __nanosleep(ns);
                     __threadfence();
                 } else {
-                    while ((g1 = *(volatile uint32_t *)(a.ring + (k - n_groups))) == 0u) __nanosleep(256);
+                    for (uint32_t ns = 256; (g1 = *(volatile uint32_t *)(a.ring + (k - n_groups))) == 0u;
+                         ns = ns < Q4_SPIN_MAX ? 2 * ns : ns)
+                        __nanosleep(ns);
                     __threadfence();
                     ch = *(volatile uint32_t *)(a.task_done + (g1 - 1u));
                 }

@@ -240,7 +240,7 @@ __device__ __noinline__ uint32_t check_structure(WS<P> s, int r, uint32_t nCU, u
     return __reduce_or_sync(FULL, bad);
 }
 
-template <class P, int MINB>
+template <class P, int MINB, bool CM>
 __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
 {
     typedef typename P::F F;
@@ -565,12 +565,40 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                 dst[5 * R + t] = lv ? P::sgn(w) : 0;
             }
         };
+        // a strict improvement goes to the verify queue (rank rows only)
+        auto enqueue = [&](uint32_t &flags) {
+            flags |= 8u;
+            bump(RC_IMPR, 1);
+            unsigned slot = 0;
+            if (lane == 0) slot = atomicAdd(a.q_count, 1u);
+            slot = __shfl_sync(FULL, slot, 0);
+            if (slot < a.q_cap) {
+                store_rows(a.q_planes + (size_t)slot * FG_PLANES * R, r);
+                if (lane == 0) {
+                    fg_qmeta qm;
+                    qm.walker = wk; qm.step = step; qm.rank = r; qm.ok = -1;
+                    qm.ff[0] = qm.ff[1] = qm.ff[2] = -1; qm.pad = 0;
+                    a.q_meta[slot] = qm;
+                }
+            } else if (lane == 0) {
+                atomicAdd(a.q_overflow, 1u);
+                hp->pad |= 1;
+            }
+        };
         auto nnz_all = [&]() -> int {
             int v = 0;
 #pragma unroll 1
             for (int l = lane; l < r; l += 32) v += P::popd(s.key(0, l)) + P::popd(s.key(1, l)) + P::popd(s.key(2, l));
             return (int)__reduce_add_sync(FULL, (uint32_t)v);
         };
+
+        // R24 (complexity mode, CM: WalkArgs::mode == 1): flips only, best by (rank, naive additions);
+        // flips skip R12 there, so the dirty set no longer covers every reducible pair
+        int nnz_cur = 0;
+        if (CM) {
+            nnz_cur = nnz_all();
+            dover = true;
+        }
 
         int boff = PXT;
         const uint32_t nsteps = (uint32_t)a.steps;
@@ -726,6 +754,8 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     const F zbF = P::sel(Z == 2 && sgb, P::neg(zb), zb);
                     const F ny = P::add(yaF, P::sel(sneg, P::neg(ybF), ybF), v);   // y_a + s y_b
                     const F nz = P::sub(zbF, zaF, v);                              // z_b - z_a
+                    // R24: no reduction edges -> a draw making a factor zero is rejected
+                    if (CM) v = v && !P::zero(ny) && !P::zero(nz);
                     const uint32_t vb = __ballot_sync(FULL, v);
                     if (!vb) {
                         draws += (kf - at) < (uint32_t)ND ? (int)(kf - at) : ND;
@@ -757,6 +787,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                 const uint32_t sa = fY == 2 ? (uint32_t)fa : (s.wsg(alpha) ^ (uint32_t)fa);
                 const uint32_t sb = fZ == 2 ? (uint32_t)fb : (s.wsg(beta) ^ (uint32_t)fb);
                 const F oY = s.key(fY, alpha), oZ = s.key(fZ, beta);
+                if (CM) nnz_cur += P::popd(kY) + P::popd(kZ) - P::popd(oY) - P::popd(oZ);
                 // R12 test keys: alpha after the commit = (AX, kY, AZ), beta = (AX, BY, kZ)
                 // (alpha and beta share the X key: they are in one X class)
                 const F AX = s.key(fX, alpha), AZ = s.key(fZ, alpha), BY = s.key(fY, beta);
@@ -840,7 +871,23 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
             }
 
             uint32_t exp_flag = 0;
-            if (!ok) {
+            if (CM) {
+                // ---- R24 step: flips only; best by (rank, naive additions) ----
+                if (ok) {
+                    c_flips++;
+                    flags |= 1u;
+                    const int adds = nnz_cur - 2 * r - a.mp;
+                    const bool better = r < best || (r == best && adds < best_adds);
+                    if (better || (r == best && adds == best_adds && (bern & 1u))) {
+                        store_rows(bw, r > best ? r : best);
+                        best = r;
+                        best_adds = adds;
+                        bump(RC_COPY, 1);
+                        flags |= 4u;
+                        if (better) enqueue(flags);
+                    }
+                }
+            } else if (!ok) {
                 // expand; continue
                 exp_flag = 2u;
             } else {
@@ -856,25 +903,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                     best_adds = nnz_all() - 2 * r - a.mp;
                     bump(RC_COPY, 1);
                     flags |= 4u;
-                    if (strict) {
-                        flags |= 8u;
-                        bump(RC_IMPR, 1);
-                        unsigned slot = 0;
-                        if (lane == 0) slot = atomicAdd(a.q_count, 1u);
-                        slot = __shfl_sync(FULL, slot, 0);
-                        if (slot < a.q_cap) {
-                            store_rows(a.q_planes + (size_t)slot * FG_PLANES * R, r);   // verifier reads rank rows
-                            if (lane == 0) {
-                                fg_qmeta qm;
-                                qm.walker = wk; qm.step = step; qm.rank = r; qm.ok = -1;
-                                qm.ff[0] = qm.ff[1] = qm.ff[2] = -1; qm.pad = 0;
-                                a.q_meta[slot] = qm;
-                            }
-                        } else if (lane == 0) {
-                            atomicAdd(a.q_overflow, 1u);
-                            hp->pad |= 1;
-                        }
-                    }
+                    if (strict) enqueue(flags);
                 }
                 // ---- PAPER:315-317 reduce (R15) ----
                 if (bern & 2u) {
@@ -891,7 +920,7 @@ __global__ void __launch_bounds__(32, MINB) walk_wl(WalkArgs a, int nwd)
                 bump(RC_EOK, ex);
                 bump(RC_EREJ, !ex);
             }
-            const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)best << 10) | ((uint64_t)flags << 20) |
+            const uint64_t ev = (uint64_t)(uint32_t)r | ((uint64_t)(uint32_t)(CM ? (best_adds & 1023) : best) << 10) | ((uint64_t)flags << 20) |
                                 ((uint64_t)alpha << 32) | ((uint64_t)beta << 42) | ((uint64_t)draws << 52);
             digest = (digest ^ ev) * 0x100000001b3ULL;
             digest ^= digest >> 32;
@@ -964,21 +993,21 @@ template <class P> size_t wl_smem(int nwd)
            3 * 32 * nwd * 2;
 }
 
-template <class P, int MINB>
+template <class P, int MINB, bool CM = false>
 cudaError_t launch_wl_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
     const int nwd = (a.R + 31) / 32;
     if (nwd > 16) return cudaErrorInvalidValue;
     const size_t smem = wl_smem<P>(nwd);
-    cudaError_t e = cudaFuncSetAttribute(walk_wl<P, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(walk_wl<P, MINB, CM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int bps = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_wl<P, MINB>, 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, walk_wl<P, MINB, CM>, 32, smem);
     if (e != cudaSuccess) return e;
     if (bps < 1) bps = 1;
     int64_t blocks = (int64_t)num_sms * bps;
     if (blocks > a.num_walkers) blocks = a.num_walkers;
-    walk_wl<P, MINB><<<(unsigned)blocks, 32, smem, st>>>(a, nwd);
+    walk_wl<P, MINB, CM><<<(unsigned)blocks, 32, smem, st>>>(a, nwd);
     return cudaGetLastError();
 }
 
@@ -991,6 +1020,8 @@ cudaError_t launch_wl_m(const WalkArgs &a, int num_sms, cudaStream_t st)
 template <class P>
 cudaError_t launch_wl(const WalkArgs &a, int num_sms, cudaStream_t st)
 {
+    // R24 runs with the largest register budget (not a throughput path)
+    if (a.mode == 1) return launch_wl_m<P, 11, true>(a, num_sms, st);
     const char *ev = getenv("FG_WL_MINB");
     int mb = ev ? atoi(ev) : 0;
     if (mb == 0) {

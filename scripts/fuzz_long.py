@@ -78,6 +78,7 @@ for family in ("q4", "w32", "ql", "wl", "wm"):
         prm = dict(k_flip=int(rng.integers(1, 17)), thr_accept_eq=int(rng.integers(0, 1 << 31)),
                    thr_reduce=int(rng.integers(0, 1 << 32)), thr_expand=int(rng.integers(0, 1 << 29)),
                    expand_slack=int(rng.integers(-1, 4)))
+        cm = rng.random() < 0.2          # R24 (naive-complexity) mode on a fifth of the runs
         W = int(rng.choice([17, 64, 203, 600, 2100]))
         steps = int(rng.integers(200, 1500))
         seed = int(rng.integers(1, 1 << 62))
@@ -88,7 +89,7 @@ for family in ("q4", "w32", "ql", "wl", "wm"):
             g = fg.FlipGraph(m, n, p, ring, R, W, 0, 0, st)
             kname = g.kernel_name
             g.seed_naive()
-            params = fg.params_default(phase_steps=steps // 2 + 1, **prm)
+            params = fg.params_default(phase_steps=steps // 2 + 1, flags=fg.FG_FLAG_COMPLEXITY if cm else 0, **prm)
             g.walk(steps, seed, params)
             got = g.get_walkers()
             g.close()
@@ -99,12 +100,12 @@ for family in ("q4", "w32", "ql", "wl", "wm"):
                 else:
                     os.environ[k] = v
         ids = np.array(sorted(set([0, W - 1] + [int(x) for x in rng.integers(0, W, size=6)])), dtype=np.int64)
-        op = OracleParams.default(**prm)
+        op = OracleParams.default(mode=1 if cm else 0, **prm)
         ref = orc.run_walkers(m, n, p, ring, R, 0, 0, steps, seed, params=op, ids=ids)
         diff = [k for k in ("r", "best_r", "digest", "cnt", "rows", "best") if not np.array_equal(got[k][ids], ref[k])]
         tot += 1
         bad += bool(diff)
         print(f"{family:3s} {(m, n, p)} ring {ring} R {R:3d} W {W:5d} steps {steps:5d} {kname:16s} "
-              f"env {env} params {prm}: {'OK' if not diff else 'DIFF ' + ','.join(diff)}", flush=True)
+              f"env {env} params {prm}{' R24' if cm else ''}: {'OK' if not diff else 'DIFF ' + ','.join(diff)}", flush=True)
 print(f"{tot - bad}/{tot} configurations bit-exact ({time.time() - t_start:.0f} s)")
 sys.exit(1 if bad else 0)

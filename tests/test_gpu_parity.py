@@ -299,6 +299,45 @@ def test_complexity_mode_parity(fg, orc, case):
     assert bb["additions"] == int(got["best_adds"].min()) and fg.fg_verify(m, n, p, ring, bb["coeffs"])[0] == 0
 
 
+@pytest.mark.parametrize("case", [((5, 5, 5), ZT, 160, 40, None), ((5, 5, 5), Z2, 144, 40, None),
+                                  ((3, 4, 12), ZT, 160, 24, None), ((4, 4, 4), ZT, 96, 40, "wm")],
+                         ids=lambda c: f"{c[0]}-{'ZT' if c[1] == 0 else 'Z2'}-R{c[2]}-{c[4] or 'default'}")
+def test_complexity_mode_wide_and_mode_switch(fg, orc, monkeypatch, case):
+    """R24 on walk_wl's formats (R > 128, wide factors; walk_ql contexts too) and on the
+    forced round-1 kernel: two R24 launches (the second resumes walk_wl's class image),
+    then a plain Alg. 1 walk on the same walkers -- R24 flips skip R12, so the image's
+    dirty set must force a full R15 scan; every sampled walker bit-exact with the
+    oracle walker run through the same three calls."""
+    (m, n, p), ring, R, W, env = case
+    if env:
+        monkeypatch.setenv("FG_WALK_KERNEL", env)
+    w = orc.walker(m, n, p, ring, R, walker_id=7)
+    w.seed_naive()
+    w.walk(4000, 123)
+    start = w.rows(0)
+    g = _ctx(fg, m, n, p, ring, R, W, base=21)
+    g.seed_pool(start)
+    cm = fg.params_default(flags=fg.FG_FLAG_COMPLEXITY)
+    g.walk(700, 77, cm)
+    g.walk(500, 78, cm)
+    mid = g.get_walkers()
+    g.walk(900, 79)
+    got = g.get_walkers()
+    a0 = orc.additions(m, n, p, start)
+    for k in sample_walkers(W, 6, seed=3):
+        o = orc.walker(m, n, p, ring, R, walker_id=21 + int(k))
+        o.seed_rows(start)
+        o.walk(700, 77, OracleParams.default(mode=1))
+        o.walk(500, 78, OracleParams.default(mode=1))
+        assert o.digest == mid["digest"][k] and o.best_adds == mid["best_adds"][k] <= a0
+        assert mid["r"][k] == start.shape[0]
+        o.walk(900, 79)
+        assert o.digest == got["digest"][k] and o.r == got["r"][k] and o.best_r == got["best_r"][k]
+        assert np.array_equal(o.rows(), got["rows"][k][: o.r])
+        assert np.array_equal(o.rows(1), got["best"][k][: o.best_r])
+    assert g.stats()["verify_fail"] == 0
+
+
 def test_best_adds_tracks_best_scheme_in_walk_mode(fg, orc):
     g = _ctx(fg, 3, 3, 3, ZT, 32, 512)
     g.seed_naive()
