@@ -34,6 +34,9 @@ using namespace fgd;
 
 #define QL_THREADS 64                  // 2-warp CTAs: one 1 KB CTA reserve per 2 warps
 #define QL_MINB 7
+#ifndef QL_SPIN_MAX
+#define QL_SPIN_MAX 0                  // a warp waiting for a group's previous chunk: 0 = busy poll,
+#endif                                 // else sleep 64 ns doubling up to this
 
 namespace {
 
@@ -70,7 +73,9 @@ __global__ void __launch_bounds__(QL_THREADS, QL_MINB) walk_ql(WalkArgs a)
     const uint32_t chunk = (uint32_t)(task / (uint64_t)n_groups);
     if (chunk > 0) {
         if (lane == 0)
-            while (*(volatile uint32_t *)(a.task_done + grp) < chunk) {}
+            for (uint32_t ns = 64; *(volatile uint32_t *)(a.task_done + grp) < chunk;
+                 ns = (int)ns < QL_SPIN_MAX ? 2 * ns : ns)
+                if (QL_SPIN_MAX) __nanosleep(ns);
         __syncwarp();
         __threadfence();
     }
