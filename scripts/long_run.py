@@ -5,7 +5,7 @@ improvements' step indices, fg_rank_first_steps), the best scheme is re-verified
 host (fg_verify, exact integer Brent check) and written with its invariants.
 
   python scripts/long_run.py <workload | m,n,p,ring,R,walkers[,target]> <seconds> <out.json>
-                             [restart_every_phases slack]
+                             [restart_every_phases slack [k_flip]]
 
 With a restart period, every that many phases the box-wide best becomes the pool
 (fg_export_best -> fg_import_best) and walkers whose best rank exceeds it by more than
@@ -30,6 +30,8 @@ def main():
     key, budget, out = sys.argv[1], float(sys.argv[2]), sys.argv[3]
     every = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     slack = int(sys.argv[5]) if len(sys.argv) > 5 else 2
+    k_flip = int(sys.argv[6]) if len(sys.argv) > 6 else 0       # 0: the default K (R11)
+    params = fg.params_default(k_flip=k_flip) if k_flip else None
     restarted = 0
     if key in WORKLOADS:
         wl = WORKLOADS[key]
@@ -48,7 +50,7 @@ def main():
     while sum(phase_ms) < budget * 1000.0:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        g.walk(S, wl.seed)
+        g.walk(S, wl.seed, params)
         e1.record(stream)
         torch.cuda.synchronize()
         phase_ms.append(e0.elapsed_time(e1))
@@ -69,7 +71,7 @@ def main():
     res = {"workload": wl.name, "walkers": wl.walkers, "phase_steps": S, "phases": len(phase_ms),
            "device_s": round(sum(phase_ms) / 1000.0, 3), "wall_s": round(time.time() - t0, 1),
            "walker_steps_per_s": wl.walkers * S * len(phase_ms) / (sum(phase_ms) / 1000.0),
-           "kernel": g.kernel_name, "restart": {"every_phases": every, "slack": slack, "restarted": restarted},
+           "kernel": g.kernel_name, "k_flip": k_flip or 16, "restart": {"every_phases": every, "slack": slack, "restarted": restarted},
            "time_to_rank_s": {str(k): round(v[0], 4) for k, v in sorted(lad.items())},
            "steps_to_rank": {str(k): v[1] for k, v in sorted(lad.items())},
            "best": {"rank": b["rank"], "additions": b["additions"], "walker_id": b["walker_id"],
