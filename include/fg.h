@@ -42,6 +42,7 @@ extern "C" {
 
 #define FG_MAX_LEN  64    /* a factor has <= 64 elements (one u64 word) */
 #define FG_MAX_RCAP 512   /* rows reserved per walker (R1) */
+#define FG_MAX_KFLIP 64   /* flip draws per step (R11: draw a uses Philox slot 7 + a, a >= 1) */
 #define FG_NCNT     12    /* per-walker counters, see fg_get_walkers */
 
 enum fg_ring { FG_ZT = 0, FG_Z2 = 1 };
@@ -61,7 +62,7 @@ enum fg_status {
    an event with probability q fires when a Philox word x satisfies x < q*2^32
    (reading R9).  fg_params_default() fills the defaults of DESIGN.md. */
 typedef struct fg_params {
-    uint32_t k_flip;        /* max flip draws per step, 1..16 (R11); default 16 */
+    uint32_t k_flip;        /* max flip draws per step, 1..FG_MAX_KFLIP (R11); default 16 */
     uint32_t thr_accept_eq; /* equal-rank acceptance, "random() < 0.01": 42949672 */
     uint32_t thr_reduce;    /* p_reduce: default 0.5 -> 2147483648 */
     uint32_t thr_expand;    /* p_expand: default 0.01 -> 42949672 */

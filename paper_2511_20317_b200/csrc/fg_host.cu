@@ -593,7 +593,7 @@ int fg_walk(fg_ctx *c, uint64_t steps, uint64_t seed, const fg_params *prm)
     if (!c->seeded) return FG_E_STATE;
     fg_params P;
     if (prm) P = *prm; else fg_params_default(&P);
-    if (P.k_flip < 1 || P.k_flip > 16 || (P.flags & ~FG_FLAG_COMPLEXITY) || P.expand_slack < -FG_MAX_RCAP)
+    if (P.k_flip < 1 || P.k_flip > FG_MAX_KFLIP || (P.flags & ~FG_FLAG_COMPLEXITY) || P.expand_slack < -FG_MAX_RCAP)
         return FG_E_ARG;
     CK(cudaSetDevice(c->device));
     WalkArgs a;

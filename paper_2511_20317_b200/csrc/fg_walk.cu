@@ -388,18 +388,19 @@ __global__ void __launch_bounds__(W32_THREADS, W32_MINB) walk_w32(WalkArgs a)
                 const uint32_t x = pw[lane == 0 ? 0 : (lane < 5 ? 3 + lane : 0)];
                 unsigned win = __ballot_sync(FULL, eval(x) && lane < na);
                 int base = 0;
-                if (!win && kf > 5) {
-                    // draws 5..15: slots 12..22 = Philox blocks 3,4,5 of this step
+                // draws 5..K-1, 32 per round: lane L evaluates draw base + L (slot 7 + draw,
+                // Philox block slot >> 2 computed per lane)
+#pragma unroll 1
+                for (int b5 = 5; !win && b5 < (int)kf; b5 += 32) {
                     uint32_t o0, o1, o2, o3;
-                    philox_block(seed, step, wid, 3u + (lane < 3 ? lane : 0), o0, o1, o2, o3);
-                    const int att = 5 + lane;                       // slot 7 + att
-                    const int src = (att + 7 - 12) >> 2, w = (att + 7) & 3;
-                    const uint32_t w0 = __shfl_sync(FULL, o0, src & 3), w1 = __shfl_sync(FULL, o1, src & 3);
-                    const uint32_t w2 = __shfl_sync(FULL, o2, src & 3), w3 = __shfl_sync(FULL, o3, src & 3);
-                    const uint32_t xb = w == 0 ? w0 : (w == 1 ? w1 : (w == 2 ? w2 : w3));
+                    const int att = b5 + lane;
+                    const uint32_t slot = 7u + (uint32_t)att;
+                    philox_block(seed, step, wid, slot >> 2, o0, o1, o2, o3);
+                    const uint32_t w = slot & 3u;
+                    const uint32_t xb = w == 0 ? o0 : (w == 1 ? o1 : (w == 2 ? o2 : o3));
                     win = __ballot_sync(FULL, eval(xb) && att < (int)kf);
-                    base = 5;
-                    draws = 5;
+                    base = b5;
+                    draws = b5;
                 }
                 if (win) {
                     const int src = __ffs(win) - 1;

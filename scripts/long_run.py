@@ -31,6 +31,10 @@ def main():
     every = int(sys.argv[4]) if len(sys.argv) > 4 else 0
     slack = int(sys.argv[5]) if len(sys.argv) > 5 else 2
     k_flip = int(sys.argv[6]) if len(sys.argv) > 6 else 0       # 0: the default K (R11)
+    run(key, budget, out, every, slack, k_flip)
+
+
+def run(key, budget, out, every=0, slack=2, k_flip=0, seed_coeffs=None, seed_note="naive"):
     params = fg.params_default(k_flip=k_flip) if k_flip else None
     restarted = 0
     if key in WORKLOADS:
@@ -44,7 +48,10 @@ def main():
     S = 10000 if wl.r_cap <= 32 else PHASE_MULTI
     stream = torch.cuda.current_stream()
     g = fg.FlipGraph(wl.m, wl.n, wl.p, wl.ring, wl.r_cap, wl.walkers, 0, 0, stream.cuda_stream)
-    g.seed_naive()
+    if seed_coeffs is None:
+        g.seed_naive()
+    else:
+        g.seed_pool(seed_coeffs)
     phase_ms, trace = [], []
     t0 = time.time()
     while sum(phase_ms) < budget * 1000.0:
@@ -63,7 +70,8 @@ def main():
                           "best_additions": b["additions"]})
     first = [int(x) for x in g.rank_first_steps(wl.r_cap)]
     naive = wl.m * wl.n * wl.p
-    lad = ladder_from_first(first, phase_ms, S, naive, seeded_rank=naive)
+    seeded = naive if seed_coeffs is None else int(seed_coeffs.shape[0])
+    lad = ladder_from_first(first, phase_ms, S, naive, seeded_rank=seeded)
     b = g.best()
     rc, ff = fg.fg_verify(wl.m, wl.n, wl.p, wl.ring, b["coeffs"])
     t, sums = fg.fg_type_invariant(wl.m, wl.n, wl.p, wl.ring, b["coeffs"])
@@ -71,7 +79,7 @@ def main():
     res = {"workload": wl.name, "walkers": wl.walkers, "phase_steps": S, "phases": len(phase_ms),
            "device_s": round(sum(phase_ms) / 1000.0, 3), "wall_s": round(time.time() - t0, 1),
            "walker_steps_per_s": wl.walkers * S * len(phase_ms) / (sum(phase_ms) / 1000.0),
-           "kernel": g.kernel_name, "k_flip": k_flip or 16, "restart": {"every_phases": every, "slack": slack, "restarted": restarted},
+           "seed": seed_note, "kernel": g.kernel_name, "k_flip": k_flip or 16, "restart": {"every_phases": every, "slack": slack, "restarted": restarted},
            "time_to_rank_s": {str(k): round(v[0], 4) for k, v in sorted(lad.items())},
            "steps_to_rank": {str(k): v[1] for k, v in sorted(lad.items())},
            "best": {"rank": b["rank"], "additions": b["additions"], "walker_id": b["walker_id"],

@@ -282,3 +282,29 @@ def test_q4_chunked_complexity_mode(fg, orc):
                           params=OracleParams.default(mode=1))
     _check(got, ref, None)
     assert np.all(got["r"] == start.shape[0])
+
+
+@pytest.mark.parametrize("kernel,fmt,R,W", [("q4", (2, 2, 8), 32, 203), ("w32", (2, 2, 8), 32, 203),
+                                            ("ql", (2, 2, 8), 48, 203), ("wl", (3, 4, 12), 160, 48),
+                                            ("wm", (3, 4, 12), 160, 48)],
+                         ids=lambda v: str(v) if not isinstance(v, tuple) else ",".join(map(str, v)))
+def test_large_flip_budget(fg, orc, kernel, fmt, R, W):
+    """K = 64 flip draws per step (R11, draws beyond 16 from Philox slots 23..70): formats
+    with wide V/W factors, where all 16 draws of a step overflow {-1,0,1} a few % of the time
+    (witness: the K = 16 oracle run on the same walkers has failed flips), every kernel
+    family bit-exact with the oracle."""
+    m, n, p = fmt
+    steps, seed = 3000, 0x5EED64
+    ids = sample_walkers(W, 8, seed=11)
+    ref16 = orc.run_walkers(m, n, p, ZT, R, 0, 0, steps, seed, params=OracleParams.default(k_flip=16), ids=ids)
+    assert ref16["cnt"][:, 3].sum() > 0
+    g = _ctx(fg, kernel, m, n, p, ZT, R, W)
+    g.seed_naive()
+    g.walk(steps, seed, fg.params_default(k_flip=64, phase_steps=1000))
+    got = g.get_walkers()
+    ref = orc.run_walkers(m, n, p, ZT, R, 0, 0, steps, seed, params=OracleParams.default(k_flip=64), ids=ids)
+    _check(got, ref, ids)
+    assert g.stats()["verify_fail"] == 0
+    with pytest.raises(fg.FgError):
+        g.walk(10, seed, fg.params_default(k_flip=65))
+    g.close()
