@@ -910,6 +910,11 @@ cudaError_t launch_q4_m(const WalkArgs &a, int num_sms, cudaStream_t st)
         e = cudaMemsetAsync(b.ring, 0, sizeof(uint32_t) * (size_t)(groups * b.chunks), st);
         if (e != cudaSuccess) return e;
         blocks = resident / Q4_WARPS;
+        // FG_Q4_SPARE (A/B): warps beyond one per group, default every resident warp
+        if (const char *sv = getenv("FG_Q4_SPARE")) {
+            const int64_t w = groups + strtol(sv, nullptr, 10);
+            if (w >= groups && w < resident) blocks = (w + Q4_WARPS - 1) / Q4_WARPS;
+        }
     } else {
         blocks = (groups + Q4_WARPS - 1) / Q4_WARPS;
     }
