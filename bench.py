@@ -51,14 +51,14 @@ def parse():
 # (kernel, workload) -> (dram bytes per launch, profile it comes from)
 # and the capture's issue / ALU-pipe utilisation (the north star's "% int-issue" figures)
 NCU_TRAFFIC = {
-    ("walk_q4<P16>", "c2_333_zt"): (54.130432e6 + 30.0288e6, "profiles/r02_ncu_walk_q4_c2_333_zt.txt", 58.37, 52.1),
-    ("walk_q4<PZ2>", "c2_333_z2"): (28.580608e6 + 34.312704e6, "profiles/r02_ncu_walk_q4_c2_333_z2.txt", 52.10, 42.2),
+    ("walk_q4<P16>", "c2_333_zt"): (54.7328e6 + 28.400896e6, "profiles/r02_ncu_walk_q4_c2_333_zt.txt", 58.84, 52.7),
+    ("walk_q4<PZ2>", "c2_333_z2"): (28.868096e6 + 32.758528e6, "profiles/r02_ncu_walk_q4_c2_333_z2.txt", 52.35, 42.6),
     ("walk_ql<P16>", "c3_444_zt"): (76.071424e6 + 60.55424e6, "profiles/r02_ncu_walk_ql_c3_444_zt.txt", 51.59, 51.0),
     ("walk_ql<PZ2>", "c3_444_z2"): (49.316096e6 + 51.712768e6, "profiles/r02_ncu_walk_ql_c3_444_z2.txt", 53.40, 53.5),
-    ("walk_wl<P32>", "c4_555_zt"): (180.3584e6 + 138.653952e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 74.21, 74.8),
+    ("walk_wl<P32>", "c4_555_zt"): (180.075264e6 + 136.5504e6, "profiles/r02_ncu_walk_wl_c4_555_zt.txt", 72.77, 76.0),
     ("walk_wl<P64>", "c5_4512_zt"): (203.328512e6 + 96.339968e6, "profiles/r02_ncu_walk_wl_c5_4512_zt.txt", 58.76, 68.2),
     ("walk_wl<P64>", "c5_5610_zt"): (245.70112e6 + 132.997376e6, "profiles/r02_ncu_walk_wl_c5_5610_zt.txt", 53.49, 66.2),
-    ("walk_wl<P64>", "c5_679_zt"): (310.861312e6 + 186.3488e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 48.24, 60.1),
+    ("walk_wl<P64>", "c5_679_zt"): (310.14528e6 + 180.666624e6, "profiles/r02_ncu_walk_wl_c5_679_zt.txt", 48.21, 61.5),
 }
 
 
