@@ -75,7 +75,7 @@ for family in ("q4", "w32", "ql", "wl", "wm"):
         if time.time() - t_start > BUDGET:
             break
         (m, n, p), ring, R = draw_format(family)
-        prm = dict(k_flip=int(rng.integers(1, 17)), thr_accept_eq=int(rng.integers(0, 1 << 31)),
+        prm = dict(k_flip=int(rng.integers(1, 17) if rng.random() < 0.75 else rng.integers(17, 65)), thr_accept_eq=int(rng.integers(0, 1 << 31)),
                    thr_reduce=int(rng.integers(0, 1 << 32)), thr_expand=int(rng.integers(0, 1 << 29)),
                    expand_slack=int(rng.integers(-1, 4)))
         cm = rng.random() < 0.2          # R24 (naive-complexity) mode on a fifth of the runs
