@@ -439,7 +439,8 @@ def main():
                "data": "synthetic",
                "config": {"workload": wl.name, "walkers_per_gpu": W, "phase_steps": S,
                           "seed": hex(wl.seed), "l2": "flushed (256 MB write) between timed steps",
-                          "kernel": roofline["kernel"]},
+                          "kernel": roofline["kernel"],
+                          "alg1": "K=16 flip draws, p_eq=0.01, p_reduce=0.5, p_expand=0.01, slack 2 (DESIGN R11, sec. 10)"},
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                "gpu_launches": int(st1["launches"] - st0["launches"]),
                "clocks": clk,
