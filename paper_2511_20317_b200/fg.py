@@ -282,7 +282,7 @@ class FlipGraph:
         self.ctx = ctx
 
     def close(self):
-        if getattr(self, "ctx", None):
+        if getattr(self, "ctx", None) and _lib is not None:   # _lib is None during interpreter shutdown
             _lib.fg_destroy(self.ctx)
             self.ctx = None
 
